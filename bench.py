@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: Newton-solve wall time of the 7.7M-DOF Neo-Hookean tensile box (BASELINE config 3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 136]
+
+A step is one full ``newton_solve`` from U = 0 (default reference tolerances) on
+generate_box_mesh(n, n, n, 1, 1, 1), z=0 clamped, u_z = 0.02 on z=1 (2 % stretch):
+residual + CSR Jacobian assembly + device BiCGSTAB per Newton iteration, all inputs
+resident in HBM.  `e2e` is the same solve through the public API with host buffers
+(U0 from pinned host memory in, U to host out).  Inputs (CSR values 4.9 GB) are far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+--impl reference times the reference algorithm on the host CPU (the numpy/numba oracle
+port of gradfem, all host threads) on a bounded sample and extrapolates to the same
+config; it prints the same metric.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # BLAS oversubscription
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Newton-solve wall time @7.7M DOF HEX8 (NH tensile box 136^3)"
+UNIT = "s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=136)
+    p.add_argument("--stretch", type=float, default=0.02)
+    p.add_argument("--cpu-sample-n", type=int, default=12)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def config(n, stretch):
+    nn = (n + 1) ** 3
+    return {"workload": f"NeoHookean tensile box {n}^3 HEX8, {stretch:.0%} stretch, newton_solve default tol",
+            "n_cells": n ** 3, "n_dofs": 3 * nn, "nnz": 9 * (3 * n + 1) ** 3, "material": "E=70e3 nu=0.3",
+            "l2_flush": "inputs (CSR values) >> 126 MB L2"}
+
+
+# ------------------------------------------------------------------ CPU reference sample
+def cpu_reference_sample(n_s, n_target, stretch):
+    """Reference algorithm on the host (oracle port of gradfem: numpy element kernels,
+    numba prange CSR matvec = kernels.py:21-28, BiCGSTAB = solvers.py:87-167) on an n_s^3
+    sample of the same problem; phase rates extrapolated to n_target^3."""
+    import oracle as orc
+    try:
+        import numba
+    except Exception:
+        numba = None
+    nodes, cells = orc.box_mesh(n_s, n_s, n_s, 1.0, 1.0, 1.0)
+    law = orc.Law("nh", E=70e3, nu=0.3, sigma_yield=250.0)
+    bot = np.flatnonzero(np.abs(nodes[:, 2]) <= 1e-5)
+    top = np.flatnonzero(np.abs(nodes[:, 2] - 1.0) <= 1e-5)
+    dd = np.concatenate([bot * 3 + c for c in range(3)] + [top * 3 + 2])
+    dv = np.concatenate([np.zeros(3 * bot.size), np.full(top.size, stretch)])
+    o = np.argsort(dd)
+    prob = orc.OracleProblem(nodes, cells, law, dd[o], dv[o])
+    U0 = np.zeros(prob.n_dofs)
+    x = np.random.default_rng(0).standard_normal(prob.n_dofs)
+    K = orc.jacobian(prob, U0)
+    orc.csr_matvec(prob.indptr, prob.indices, K, x)  # numba JIT outside the timing
+    threads = 1
+    if numba is not None:  # pick the fastest thread count (oversubscribed hosts spin badly)
+        best = None
+        cands = sorted({t for t in (1, 2, 4, 8, 16, 32, 64, 128) if t <= os.cpu_count()} | {os.cpu_count()})
+        for th in cands:
+            numba.set_num_threads(min(th, numba.config.NUMBA_NUM_THREADS))
+            orc.csr_matvec(prob.indptr, prob.indices, K, x)
+            t0 = time.perf_counter()
+            for _ in range(5):
+                orc.csr_matvec(prob.indptr, prob.indices, K, x)
+            dt = time.perf_counter() - t0
+            if best is None or dt < best[0]:
+                best = (dt, th)
+        threads = best[1]
+        numba.set_num_threads(min(threads, numba.config.NUMBA_NUM_THREADS))
+    t0 = time.perf_counter()
+    orc.residual(prob, U0)
+    t_R = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.jacobian(prob, U0)
+    t_K = time.perf_counter() - t0
+    reps = 20
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        orc.csr_matvec(prob.indptr, prob.indices, K, x)
+    t_mv = (time.perf_counter() - t0) / reps
+    stats = {}
+    t0 = time.perf_counter()
+    _, norms, its = orc.newton(prob, stats=stats)
+    t_newton = time.perf_counter() - t0
+    mv = stats.get("matvecs", 0)
+    t_vec = max(t_newton - (len(norms)) * t_R - its * t_K - mv * t_mv, 0.0)  # BiCGSTAB vector work
+    ne_s, nnz_s, n_dofs_s = cells.shape[0], prob.indices.size, prob.n_dofs
+    ne_t = n_target ** 3
+    nnz_t = 9 * (3 * n_target + 1) ** 3
+    dofs_t = 3 * (n_target + 1) ** 3
+    mv_t = mv * n_target / n_s  # BiCGSTAB iterations grow ~linearly with the mesh edge
+    vec_t = t_vec / (mv * n_dofs_s) * mv_t * dofs_t if mv else 0.0
+    est = len(norms) * t_R / ne_s * ne_t + its * t_K / ne_s * ne_t + mv_t * t_mv / nnz_s * nnz_t + vec_t
+    return {
+        "value": est, "unit": UNIT, "cores": threads, "kind": "port",
+        "sample": (f"oracle NH Newton on {n_s}^3 ({n_dofs_s} DOF) in {t_newton:.2f}s: {its} Newton its, "
+                   f"{mv} matvecs; R {t_R / ne_s * 1e6:.1f} us/cell, K {t_K / ne_s * 1e6:.1f} us/cell, "
+                   f"SpMV {nnz_s * 12 / t_mv / 1e9:.1f} GB/s ({threads} thr); extrapolated to {n_target}^3 with "
+                   f"{mv_t:.0f} matvecs (x n/n_s)"),
+        "sample_wall_s": t_newton,
+    }
+
+
+# ----------------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-i", os.environ.get("LOCAL_RANK", "0"), "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_2212_00964_b200 as fem
+    from paper_2212_00964_b200 import _device as D
+    from paper_2212_00964_b200 import _lib
+    from paper_2212_00964_b200.solvers import _tangent_matrix
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    n = args.n
+    mesh = fem.generate_box_mesh(n, n, n, 1.0, 1.0, 1.0)
+    alu = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+    bot, top = fem.BoundaryLocator.plane(2, 0.0), fem.BoundaryLocator.plane(2, 1.0)
+    s = args.stretch
+    specs = [fem.DirichletSpec(bot, c, lambda p: 0.0) for c in range(3)] + [
+        fem.DirichletSpec(top, 2, lambda p, s=s: np.full(np.asarray(p).shape[:-1], s) if np.ndim(p) > 1 else s)]
+    prob = fem.NeoHookeanProblem(mesh, alu, specs)
+    t0 = time.perf_counter()
+    ws = fem.workspace(prob)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    N = prob.n_dofs
+    U0 = D.zeros(N)
+
+    def step():
+        return fem.newton_solve(prob, U0)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks()
+    l0 = _lib.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    reports = []
+    ev[0].record()
+    for k in range(args.steps):
+        U, rep = step()
+        ev[k + 1].record()
+        reports.append(rep)
+    barrier()
+    launches = _lib.launch_count() - l0
+    ck = clocks.stop()
+    per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    rep = reports[-1]
+    lin_iters = [s_.iterations for s_ in rep.linear_stats]
+    matvecs = sum(s_.matvecs for s_ in rep.linear_stats)
+
+    # ---------------- kernel-level evidence (after the timed region, same stream, CUDA events)
+    K = _tangent_matrix(prob, U)
+    x = D.to_device(np.random.default_rng(0).standard_normal(N))
+    y = D.empty(N)
+    h = K._device_handle()
+    lib = _lib.lib()
+    for _ in range(3):
+        lib.b200fem_matvec(h, D.ptr(x), D.ptr(y))
+    reps = 30
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        lib.b200fem_matvec(h, D.ptr(x), D.ptr(y))
+    e1.record()
+    torch.cuda.synchronize()
+    t_spmv = e0.elapsed_time(e1) / reps / 1e3
+    nnz = ws.nnz
+    n_nodes = mesh.n_nodes
+    bytes_fem = 8 * nnz + 4 * (nnz // 9) + 4 * (n_nodes + 1) + 8 * N + 8 * N
+    bytes_csr = 12 * nnz + 4 * (N + 1) + 8 * N + 8 * N
+    R = D.empty(N)
+    e0.record()
+    for _ in range(5):
+        ws.residual(prob, U, R)
+    e1.record()
+    torch.cuda.synchronize()
+    t_res = e0.elapsed_time(e1) / 5 / 1e3
+    e0.record()
+    for _ in range(3):
+        ws.jacobian(prob, U, K.device_data)
+    e1.record()
+    torch.cuda.synchronize()
+    t_jac = e0.elapsed_time(e1) / 3 / 1e3
+
+    # ---------------- e2e through the public API with host buffers
+    U0_host = torch.zeros(N, dtype=torch.float64).pin_memory()
+    fem.newton_solve(prob, U0_host)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        Uh, _ = fem.newton_solve(prob, U0_host)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    peak, peak_kind = peaks()
+    traffic = ncu_traffic()
+    achieved = bytes_fem / t_spmv / 1e9
+    out = {
+        "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated box mesh, 2% stretch BCs)",
+        "config": dict(config(n, s), parallelism="replicas" if world > 1 else "single"),
+        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N},
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "k_spmv_fem3 (CSR SpMV, node-blocked column index)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "bytes_per_launch": bytes_fem,
+                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6},
+        "newton": {"iterations": rep.n_iterations, "residual_norms": rep.residual_norms,
+                   "linear_iterations": lin_iters, "matvecs": matvecs, "per_step_ms": per_step},
+        "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": mesh.n_cells / t_res / 1e6,
+                     "jacobian_ms": t_jac * 1e3, "jacobian_mcells_s": mesh.n_cells / t_jac / 1e6,
+                     "jacobian_hbm_gbs": (8 * nnz + 32 * mesh.n_cells + 24 * n_nodes + 8 * N) / t_jac / 1e9},
+        "setup_s": setup_s,
+        "clocks": ck,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(args.cpu_sample_n, n, s).items()
+                               if k != "sample_wall_s"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals, walls = [], []
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.cpu_sample_n, args.n, args.stretch)
+    last = None
+    for _ in range(args.steps):
+        last = cpu_reference_sample(args.cpu_sample_n, args.n, args.stretch)
+        vals.append(last["value"])
+        walls.append(last["sample_wall_s"])
+    v = float(np.mean(vals))
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(walls)) * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config(args.n, args.stretch),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    run_reference(a) if a.impl == "reference" else run_ours(a)

@@ -1,0 +1,156 @@
+/*
+ * b200fem.h — C ABI of libb200fem.so, the sm_100a forward-solve hot path of the
+ * differentiable HEX8 FEM (arXiv 2212.00964; reference package "gradfem").
+ *
+ * Conventions
+ *  - Every entry point returns int status (0 = OK, see B200FEM_E_*) and, when it
+ *    can fail for a data reason, fills a caller-provided b200fem_error.
+ *  - "host" pointers are CPU memory read during the call; "dev" pointers are
+ *    device memory (e.g. torch CUDA tensors' data_ptr()) that the library never
+ *    frees. Everything a context allocates is freed by b200fem_ctx_destroy.
+ *  - A context (and a matrix) is bound to one CUDA stream; calls are ordered on
+ *    it and are not re-entrant per handle (reference: single logical thread,
+ *    SPEC.md:452; numba threads only inside csr_matvec, kernels.py:21-28).
+ *  - DOFs are node-major (dof = node*vec + comp) exactly as the reference
+ *    (assembly.py:94); the CSR pattern / scatter map are bit-identical to
+ *    sparse.py:75-108.
+ *
+ * Each entry cites the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/gradfem/).
+ */
+#ifndef B200FEM_H
+#define B200FEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference exception classes in Python) ---- */
+#define B200FEM_OK 0
+#define B200FEM_E_INVERTED_ELEMENT 1     /* elements.py:124-129  InvertedElementError      */
+#define B200FEM_E_INVERTED_DEFORMATION 2 /* materials.py:94-100  InvertedDeformationError  */
+#define B200FEM_E_NONFINITE_VALUE 3      /* assembly.py:228-233  KernelEvaluationError     */
+#define B200FEM_E_NONFINITE_DERIV 4      /* assembly.py:219-227  KernelEvaluationError     */
+#define B200FEM_E_LINEAR_SOLVER 5        /* solvers.py:119-125   LinearSolverError         */
+#define B200FEM_E_BREAKDOWN 6            /* solvers.py:149-155   BreakdownError            */
+#define B200FEM_E_ZERO_DIAGONAL 7        /* solvers.py:102-103   LinearSolverError         */
+#define B200FEM_E_INVALID 8              /* bad argument                                   */
+#define B200FEM_E_CUDA 9                 /* CUDA runtime error                             */
+#define B200FEM_E_UNSUPPORTED 10         /* mesh/material outside the device path          */
+
+/* ---- materials (materials.py:134-194; problems.py:166-202) ---- */
+#define B200FEM_MAT_POISSON 0 /* IsotropicDiffusion: params[0] = alpha             */
+#define B200FEM_MAT_LE 1      /* LinearElastic: params[1] = lam, params[2] = mu     */
+#define B200FEM_MAT_NH 2      /* NeoHookean: params[2] = G (= mu), params[3] = kappa */
+#define B200FEM_MAT_J2 3      /* J2Plasticity: lam, mu, params[4] = sigma_yield      */
+
+#define B200FEM_FLAG_SIMP 1          /* flux scaled by theta_e^penalty, params[5] = penalty */
+#define B200FEM_FLAG_DESIGN_SOURCE 2 /* Poisson nodal design source b = sum theta_k phi_k   */
+
+typedef struct b200fem_error {
+  int32_t code;
+  int32_t qp;     /* quadrature point of the first offender, -1 if n/a   */
+  int64_t cell;   /* global cell index of the first offender, -1 if n/a  */
+  double value;   /* det / min det(F) / residual, depending on code      */
+  int64_t iterations;
+  char msg[256];
+} b200fem_error;
+
+typedef struct b200fem_solve_info {
+  int64_t iterations; /* BiCGSTAB iterations (solvers.py:131-132 counter)   */
+  int64_t matvecs;    /* operator applications incl. explicit residuals     */
+  int64_t restarts;   /* explicit-residual (re)starts                       */
+  double residual;    /* final true residual ||A x - b||                    */
+  double tol;         /* max(rel_tol * ||b||, abs_tol)                      */
+} b200fem_solve_info;
+
+typedef struct b200fem_ctx b200fem_ctx;
+typedef struct b200fem_matrix b200fem_matrix;
+
+/* ---- library ---- */
+int b200fem_version(void);
+/* number of kernels this library has launched since load (bench evidence) */
+int64_t b200fem_launch_count(void);
+/* block until all work on `stream` (cudaStream_t, 0 = legacy default) is done */
+int b200fem_stream_sync(void *stream);
+
+/* ---- context: replaces assembly.workspace() (assembly.py:83-145) ----
+ * coords_host (n_nodes,3) f64, cells_host (n_cells,8) int64 in VTK HEX8 order.
+ * Builds on the device: the geometry check (map_elements, elements.py:117-131),
+ * the node adjacency / CSR pattern / scatter positions (sparse.py:75-108),
+ * diagonal slots (assembly.py:96-97) and the cell colouring used for the
+ * deterministic reduction. */
+int b200fem_ctx_create(b200fem_ctx **out, int64_t n_nodes, int64_t n_cells, int32_t vec,
+                       const double *coords_host, const int64_t *cells_host, int32_t material,
+                       const double *params /* [8] */, int32_t flags, void *stream,
+                       b200fem_error *err);
+int b200fem_ctx_destroy(b200fem_ctx *ctx);
+int b200fem_ctx_info(const b200fem_ctx *ctx, int64_t *n_dofs, int64_t *nnz, int32_t *n_colors,
+                     int32_t *max_neighbors);
+
+/* pattern copy-outs for bit-exact parity checks (device outputs, caller-sized) */
+int b200fem_copy_indptr(b200fem_ctx *ctx, int32_t *indptr_dev /* n_dofs+1 */);
+int b200fem_copy_indices(b200fem_ctx *ctx, int32_t *indices_dev /* nnz */);
+int b200fem_copy_dest(b200fem_ctx *ctx, int64_t cell_lo, int64_t cell_hi,
+                      int32_t *dest_dev /* (cell_hi-cell_lo, 8vec, 8vec) */);
+int b200fem_copy_diag_slots(b200fem_ctx *ctx, int32_t *diag_dev /* n_dofs */);
+
+/* ---- boundary data / design / state (assembly.py:99-128, problems.py:93-163) ---- */
+int b200fem_set_dirichlet(b200fem_ctx *ctx, const int64_t *dofs_host, const double *values_host,
+                          int64_t n);
+int b200fem_set_loads(b200fem_ctx *ctx, const double *f_neumann_host /* nullable */,
+                      const double *f_body_host /* nullable */);
+/* theta: per cell (SIMP) or per node (design source); device or host pointer */
+int b200fem_set_theta(b200fem_ctx *ctx, const double *theta, int64_t n, int32_t is_host);
+int b200fem_set_state(b200fem_ctx *ctx, const double *eps_prev, const double *sig_prev,
+                      int32_t is_host); /* (n_cells,8,3,3) each */
+int b200fem_get_state(b200fem_ctx *ctx, double *eps_prev_dev, double *sig_prev_dev);
+
+/* ---- assembly (assembly.py:236-261, 273-300) ----
+ * residual: R = sum_e R_e(U) (deterministic colour-ordered reduction)
+ *           - bc_scale*f_neumann - f_body; Dirichlet rows -> U[d]-bc_scale*u_D.
+ * norm_host (nullable) receives ||R||_2 (forces a stream sync).            */
+int b200fem_residual(b200fem_ctx *ctx, const double *U_dev, double bc_scale,
+                     int32_t apply_dirichlet, double *R_dev, double *norm_host,
+                     b200fem_error *err);
+/* jacobian: CSR values (pattern of this ctx) of dR/dU with Dirichlet identity rows. */
+int b200fem_jacobian(b200fem_ctx *ctx, const double *U_dev, double *data_dev, b200fem_error *err);
+/* flux at every quadrature point (N_e,8,vec,3)  (solvers.py:237-250) */
+int b200fem_qp_flux(b200fem_ctx *ctx, const double *U_dev, double *out_dev, b200fem_error *err);
+/* volume average of the flux (vec*3 values, host)   (solvers.py:253-258) */
+int b200fem_volume_average_flux(b200fem_ctx *ctx, const double *U_dev, double *out_host,
+                                b200fem_error *err);
+/* J2 state commit eps <- sym grad u, sig <- return map (problems.py:155-163) */
+int b200fem_commit_state(b200fem_ctx *ctx, const double *U_dev);
+
+/* ---- sparse operators (sparse.py:15-51, kernels.py:37-47) ---- */
+/* FEM matrix on this ctx's pattern (uses the node-blocked index, no indices array) */
+int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *data_dev);
+/* generic CSR on the device (any square matrix with sorted unique columns) */
+int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr_dev,
+                       const int32_t *indices_dev, const double *data_dev, void *stream);
+int b200fem_matrix_set_data(b200fem_matrix *m, const double *data_dev);
+int b200fem_matrix_destroy(b200fem_matrix *m);
+int b200fem_matvec(b200fem_matrix *m, const double *x_dev, double *y_dev);
+int b200fem_diagonal(b200fem_matrix *m, double *diag_dev);
+
+/* ---- Krylov (solvers.py:87-167) ----
+ * x_dev holds x0 on entry when has_x0 != 0 (else it is zeroed) and the solution on exit.
+ * max_iters <= 0 means 10*n. Same termination, restart and breakdown rules as the reference. */
+int b200fem_bicgstab(b200fem_matrix *m, const double *b_dev, double *x_dev, int32_t has_x0,
+                     double rel_tol, double abs_tol, int64_t max_iters, b200fem_solve_info *info,
+                     b200fem_error *err);
+
+/* ---- small vector helpers (deterministic) ---- */
+int b200fem_norm2(const double *x_dev, int64_t n, double *out_host, void *stream);
+int b200fem_gather_sum(const double *x_dev, const int64_t *idx_dev, int64_t n, double *out_host,
+                       void *stream);
+int b200fem_axpy(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
+int b200fem_scale(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200FEM_H */

@@ -1,0 +1,69 @@
+"""torch is used only for device buffers and the current CUDA stream."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def device():
+    t = torch()
+    _lib.lib()  # raises DeviceUnavailableError when there is no GPU / library
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream():
+    return C.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def is_device_tensor(x) -> bool:
+    t = torch()
+    return isinstance(x, t.Tensor) and x.is_cuda
+
+
+def to_device(x, dtype=None, copy=False):
+    """numpy / torch -> contiguous CUDA tensor (float64 unless dtype given)."""
+    t = torch()
+    dt = dtype or t.float64
+    if isinstance(x, t.Tensor):
+        y = x.to(device=device(), dtype=dt)
+        y = y.contiguous()
+        return y.clone() if (copy and y.data_ptr() == x.data_ptr()) else y
+    arr = np.ascontiguousarray(np.asarray(x), dtype=_np_dtype(dt))
+    return t.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def empty(n, dtype=None):
+    t = torch()
+    return t.empty(n, dtype=dtype or t.float64, device=device())
+
+
+def zeros(n, dtype=None):
+    t = torch()
+    return t.zeros(n, dtype=dtype or t.float64, device=device())
+
+
+def to_host(x) -> np.ndarray:
+    return x.detach().cpu().numpy()
+
+
+def ptr(x):
+    return C.c_void_p(x.data_ptr())
+
+
+def hptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _np_dtype(dt):
+    t = torch()
+    return {t.float64: np.float64, t.int32: np.int32, t.int64: np.int64, t.uint8: np.uint8}[dt]

@@ -1,0 +1,249 @@
+// Internal definitions shared by the libb200fem translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b200fem.h"
+
+namespace b200 {
+
+// ---------------------------------------------------------------- launch grid
+// Reduction kernels use a FIXED grid so that every per-block partial sum, and the
+// order in which the last block combines them, is independent of the problem size
+// tiling -> results are bit-identical run to run.  148 SMs x 8 blocks of 256 threads.
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRedBlocks = 148 * 8;
+constexpr int kMaxVals = 16;  // values reduced per launch
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// -------------------------------------------------------------- error helpers
+void set_err(b200fem_error *err, int code, const char *fmt, ...);
+int cuda_status(cudaError_t e, b200fem_error *err, const char *where);
+#define B200_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) return cuda_status(_e, nullptr, #call);               \
+  } while (0)
+#define B200_CUDA_E(call, err)                                                   \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) return cuda_status(_e, err, #call);                   \
+  } while (0)
+
+// ---------------------------------------------------- device error reporting
+// Keys are cell*8+q (the reference reports the FIRST offender in (cell, qp) order,
+// assembly.py:204-213); ULLONG_MAX = none.
+struct DevErr {
+  unsigned long long inv_def;   // NH det F <= 0
+  unsigned long long nonfin_v;  // non-finite flux value
+  unsigned long long nonfin_d;  // non-finite tangent
+  unsigned long long inv_elem;  // det J <= 0 (geometry)
+  unsigned long long min_detF;  // ordered-bits min of det F over offenders
+  unsigned long long elem_det;  // ordered-bits det J of ... (min)
+};
+
+// ----------------------------------------------------------- scalar workspace
+// Device-resident reduction scratch: partials[kRedBlocks * kMaxVals], a ticket for the
+// last-block pattern and the reduced results.
+struct RedScratch {
+  double *partials;
+  unsigned int *ticket;
+  double *result;  // kMaxVals
+};
+
+// Krylov scalars live on the device so the inner loop never waits on the host.
+enum : int { KS_RUNNING = 0, KS_CONV_INNER = 1, KS_BREAKDOWN = 2, KS_MAXED = 3 };
+struct KrylovScalars {
+  double rho, alpha, omega, beta;
+  double r0v, tt, ts;
+  double res, tol;
+  long long mv;
+  double r0r0, r0r, rr;
+  long long it, max_iters;
+  int status, first;
+};
+
+struct MatParams {
+  double alpha, lam, mu, kappa, sy, penalty;
+  int simp, design_source;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_nodes = 0, n_cells = 0, n_dofs = 0, nnz = 0;
+  int vec = 1, material = 0, flags = 0;
+  MatParams mp{};
+  double *coords = nullptr;   // (n_nodes,3)
+  int32_t *cells = nullptr;   // (n_cells,8)
+  int32_t *nbr_ptr = nullptr; // (n_nodes+1) node adjacency (includes self)
+  int32_t *nbr = nullptr;     // sorted neighbour node ids
+  int32_t *indptr = nullptr;  // (n_dofs+1)
+  int32_t *indices = nullptr; // lazily materialised (vec==1 aliases nbr)
+  uint8_t *cpos = nullptr;    // (n_cells,64) position of node b in node a's neighbour list
+  int32_t *diag = nullptr;    // (n_dofs) diagonal slot
+  int max_nbr = 0;
+  // colouring (host offsets, device cell lists ordered by colour then cell id)
+  int n_colors = 0;
+  std::vector<int64_t> color_off;
+  int32_t *color_cells = nullptr;
+  // boundary data
+  int64_t n_dir = 0;
+  int32_t *dir_dofs = nullptr;
+  double *dir_vals = nullptr;
+  double *f_neumann = nullptr, *f_body = nullptr;
+  double *theta = nullptr;
+  int64_t n_theta = 0;
+  double *eps_prev = nullptr, *sig_prev = nullptr;
+  // scratch
+  DevErr *derr = nullptr;
+  RedScratch red{};
+  double *pinned = nullptr;  // host pinned scratch (8 doubles)
+};
+
+struct KrylovWork {
+  int64_t n = 0;
+  double *r = nullptr, *r0 = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr;
+  double *diag = nullptr, *inv = nullptr;
+  KrylovScalars *sc = nullptr;
+  KrylovScalars *sc_host = nullptr;  // pinned
+  RedScratch red{};
+  cudaEvent_t ev[2]{};
+};
+
+enum MatKind : int { MK_CSR = 0, MK_FEM3 = 1 };
+struct Matrix {
+  MatKind kind = MK_CSR;
+  int64_t n = 0, nnz = 0;
+  const int32_t *indptr = nullptr, *indices = nullptr;  // CSR
+  const int32_t *nbr_ptr = nullptr, *nbr = nullptr;     // FEM3
+  const int32_t *diag_slots = nullptr;                  // FEM3 (optional fast diagonal)
+  const double *data = nullptr;
+  cudaStream_t stream = nullptr;
+  int lanes = 8;  // CSR sub-warp width
+  KrylovWork *kw = nullptr;
+};
+
+// allocation helpers
+template <class T>
+inline cudaError_t dalloc(T **p, size_t n) {
+  return cudaMalloc((void **)p, (n ? n : 1) * sizeof(T));
+}
+int red_alloc(RedScratch *r);
+void red_free(RedScratch *r);
+
+// ---------------------------------------------------------------- launchers
+// reductions (deterministic): out_host may be null (result stays in r->result)
+int launch_dot(const double *x, const double *y, int64_t n, RedScratch *r, cudaStream_t s);
+int launch_gather_sum(const double *x, const int64_t *idx, int64_t n, RedScratch *r, cudaStream_t s);
+int launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s);
+int launch_scale(int64_t n, double a, const double *x, double *y, cudaStream_t s);
+
+// sparse
+enum SpmvMode : int { SP_PLAIN = 0, SP_JACOBI_R0 = 1, SP_JACOBI_TT = 2, SP_RESIDUAL = 3 };
+struct SpmvArgs {
+  const double *x;   // operand (p, s or x)
+  double *y;         // output (v, t or r)
+  const double *inv; // inverse diagonal
+  const double *dg;  // diagonal (residual mode)
+  const double *aux; // r0 (mode 1), b (mode 3)
+  double *aux2;      // r0 copy target (mode 3)
+  KrylovScalars *sc; // null -> always run
+  int stage;         // which scalar update the last block performs
+};
+int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
+int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
+
+// element kernels
+int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int apply_dirichlet,
+                    b200fem_error *err, double *norm_host);
+int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err);
+int launch_qp_flux(Ctx *c, const double *U, double *out, b200fem_error *err);
+int launch_volume_average(Ctx *c, const double *U, double *out_host, b200fem_error *err);
+int launch_commit(Ctx *c, const double *U);
+int check_geometry(Ctx *c, b200fem_error *err);
+void element_tables_init();
+int fetch_element_errors(Ctx *c, b200fem_error *err, bool jacobian);
+
+// Krylov
+int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol,
+             int64_t max_iters, b200fem_solve_info *info, b200fem_error *err);
+
+// ------------------------------------------------------------ device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of NV values per thread; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sh)[kWarps]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) sh[j][w] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double a = 0.0;
+      for (int k = 0; k < kWarps; ++k) a += sh[j][k];
+      v[j] = a;
+    }
+  }
+}
+
+// Write this block's partials; return true in ALL threads of the last block to finish,
+// which then holds the fully reduced values in `tot` (thread 0 valid).
+template <int NV>
+__device__ __forceinline__ bool block_partials_and_finish(double (&v)[NV], RedScratch red,
+                                                          double (&tot)[NV]) {
+  __shared__ double sh[NV][kWarps];
+  __shared__ bool last;
+  block_reduce<NV>(v, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) red.partials[j * kRedBlocks + blockIdx.x] = v[j];
+    __threadfence();
+    unsigned t = atomicAdd(red.ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double a = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      a += __ldcg(red.partials + j * kRedBlocks + b);
+    acc[j] = a;
+  }
+  __syncthreads();
+  block_reduce<NV>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      tot[j] = acc[j];
+      red.result[j] = acc[j];
+    }
+    *red.ticket = 0u;
+  }
+  return true;
+}
+
+}  // namespace b200

@@ -1,0 +1,337 @@
+// Jacobi-preconditioned BiCGSTAB with the reference's exact control flow
+// (solvers.py:87-167), run on the device: all recurrence scalars (rho, alpha, omega,
+// beta, the iteration counter and the status) live in device memory and are updated by
+// the last block of each reduction, so the host never waits inside the inner loop.  The
+// host C++ loop only enqueues batches of iterations and polls the status of the
+// previous batch (double buffered), reproducing the outer restart loop: explicit
+// residual check, LinearSolverError at max_iters, restart on breakdown, BreakdownError
+// when a restart makes no progress.
+//
+// Per iteration (5 launches):
+//   K_a  p = r + beta (p - omega v)                                      (solvers.py:140)
+//   K_b  v = D^-1 A p  (+ r0.v -> alpha, breakdown if 0)                  (141-143, 158)
+//   K_c  s = r - alpha v                                                  (159)
+//   K_d  t = D^-1 A s  (+ t.t, t.s -> omega)                              (160-162)
+//   K_e  x += alpha p + omega s ; r = s - omega t (+ ||D r||, r0.r, r.r)  (163-165)
+//        last block: convergence test, then the next iteration's start:
+//        it += 1, rho_new = r0.r, breakdown test, beta                   (131-139)
+
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace b200 {
+
+__device__ __forceinline__ void iter_start(KrylovScalars *S) {
+  if (S->it >= S->max_iters) {
+    S->status = KS_MAXED;
+    return;
+  }
+  S->it += 1;
+  const double rho_new = S->r0r;
+  const double scale = sqrt(S->r0r0) * sqrt(S->rr);
+  const bool broke = fabs(rho_new) <= 1e-30 * scale || (!S->first && S->omega == 0.0);
+  if (broke) {
+    S->status = KS_BREAKDOWN;
+    return;
+  }
+  S->beta = S->first ? 0.0 : (rho_new / S->rho) * (S->alpha / S->omega);
+  S->first = 0;
+  S->rho = rho_new;
+}
+
+__global__ void k_begin(KrylovScalars *S) {
+  if (S->status == KS_RUNNING) iter_start(S);
+}
+
+__global__ void __launch_bounds__(kThreads) k_update_p(int64_t n, const double *__restrict__ r,
+                                                       const double *__restrict__ v, double *__restrict__ p,
+                                                       const KrylovScalars *S) {
+  if (S->status != KS_RUNNING) return;
+  const double beta = S->beta, omega = S->omega;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * (p[i] - omega * v[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_update_s(int64_t n, const double *__restrict__ r,
+                                                       const double *__restrict__ v, double *__restrict__ s,
+                                                       const KrylovScalars *S) {
+  if (S->status != KS_RUNNING) return;
+  const double alpha = S->alpha;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s[i] = r[i] - alpha * v[i];
+}
+
+__global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                                                        const double *__restrict__ p, const double *__restrict__ s,
+                                                        const double *__restrict__ t, const double *__restrict__ r0,
+                                                        const double *__restrict__ dg, KrylovScalars *S,
+                                                        RedScratch red) {
+  if (S->status != KS_RUNNING) return;
+  const double alpha = S->alpha, omega = S->omega;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i] + omega * s[i];
+    const double ri = s[i] - omega * t[i];
+    r[i] = ri;
+    const double dr = dg[i] * ri;
+    acc[0] = fma(dr, dr, acc[0]);
+    acc[1] = fma(r0[i], ri, acc[1]);
+    acc[2] = fma(ri, ri, acc[2]);
+  }
+  double tot[3];
+  if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0) {
+    S->res = sqrt(tot[0]);
+    S->r0r = tot[1];
+    S->rr = tot[2];
+    if (S->res <= S->tol) {
+      S->status = KS_CONV_INNER;
+      return;
+    }
+    iter_start(S);
+  }
+}
+
+static int ensure_work(Matrix *m) {
+  if (m->kw) return 0;
+  KrylovWork *w = new KrylovWork();
+  w->n = m->n;
+  double **vecs[] = {&w->r, &w->r0, &w->p, &w->v, &w->s, &w->t, &w->diag, &w->inv};
+  for (double **v : vecs) B200_CUDA(dalloc(v, m->n));
+  B200_CUDA(dalloc(&w->sc, 1));
+  B200_CUDA(cudaMallocHost((void **)&w->sc_host, 3 * sizeof(KrylovScalars)));
+  if (red_alloc(&w->red)) return B200FEM_E_CUDA;
+  B200_CUDA(cudaEventCreateWithFlags(&w->ev[0], cudaEventDisableTiming));
+  B200_CUDA(cudaEventCreateWithFlags(&w->ev[1], cudaEventDisableTiming));
+  m->kw = w;
+  return 0;
+}
+
+void free_work(KrylovWork *w) {
+  if (!w) return;
+  double *vecs[] = {w->r, w->r0, w->p, w->v, w->s, w->t, w->diag, w->inv};
+  for (double *v : vecs) cudaFree(v);
+  cudaFree(w->sc);
+  cudaFreeHost(w->sc_host);
+  red_free(&w->red);
+  cudaEventDestroy(w->ev[0]);
+  cudaEventDestroy(w->ev[1]);
+  delete w;
+}
+
+static int grid_vec(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
+
+static void enqueue_iteration(Matrix *m, const double *b, double *x) {
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  const int64_t n = m->n;
+  k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
+  SpmvArgs a1{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
+  launch_spmv(m, SP_JACOBI_R0, a1, &w->red);
+  k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
+  SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
+  launch_spmv(m, SP_JACOBI_TT, a2, &w->red);
+  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red);
+  count_launch(3);
+  (void)b;
+}
+
+int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol, int64_t max_iters,
+             b200fem_solve_info *info, b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  if (info) memset(info, 0, sizeof(*info));
+  if (!(rel_tol > 0) || !(abs_tol > 0)) {
+    set_err(err, B200FEM_E_INVALID, "linear solver tolerances must be positive");
+    return B200FEM_E_INVALID;
+  }
+  int st = ensure_work(m);
+  if (st) return set_err(err, st, "Krylov workspace allocation failed"), st;
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  const int64_t n = m->n;
+  int64_t nzero = 0;
+  st = launch_diagonal(m, w->diag, w->inv, &w->red, &nzero);
+  if (st) return set_err(err, st, "diagonal extraction failed"), st;
+  if (nzero) {
+    set_err(err, B200FEM_E_ZERO_DIAGONAL, "zero diagonal entry; Jacobi preconditioner undefined");
+    return B200FEM_E_ZERO_DIAGONAL;
+  }
+  if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x, 0, n * sizeof(double), s), err);
+  if (launch_dot(b, b, n, &w->red, s)) return B200FEM_E_CUDA;
+  double bb = 0.0;
+  B200_CUDA_E(cudaMemcpyAsync(&bb, w->red.result, sizeof(double), cudaMemcpyDeviceToHost, s), err);
+  B200_CUDA_E(cudaStreamSynchronize(s), err);
+  const double tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
+  const int64_t max_it = max_iters > 0 ? max_iters : 10 * n;
+
+  KrylovScalars *H = w->sc_host;  // [0] control, [1],[2] poll buffers
+  memset(H, 0, 3 * sizeof(KrylovScalars));
+  H[0].tol = tol;
+  H[0].max_iters = max_it;
+  long long it = 0, mv = 0, restarts = 0;
+  double last_bd = -1.0;
+  const size_t ssz = sizeof(KrylovScalars);
+  for (;;) {
+    // ---- (re)start: r = D^-1 (b - A x), r0 = r, res = ||D r||   (solvers.py:115-118)
+    H[0].status = KS_RUNNING;
+    H[0].first = 1;
+    H[0].rho = H[0].alpha = H[0].omega = 1.0;
+    H[0].it = it;
+    H[0].mv = mv;
+    B200_CUDA_E(cudaMemcpyAsync(w->sc, &H[0], ssz, cudaMemcpyHostToDevice, s), err);
+    SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->r0, w->sc, 0};
+    if (launch_spmv(m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
+    ++restarts;
+    B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+    B200_CUDA_E(cudaStreamSynchronize(s), err);
+    mv = H[1].mv;
+    const double res = H[1].res;
+    if (res <= tol) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      return 0;
+    }
+    if (it >= max_it) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      if (err) {
+        err->iterations = it;
+        err->value = res;
+      }
+      set_err(err, B200FEM_E_LINEAR_SOLVER, "BiCGSTAB did not converge in %lld iterations (residual %.3e, tol %.3e)",
+              (long long)max_it, res, tol);
+      return B200FEM_E_LINEAR_SOLVER;
+    }
+    B200_CUDA_E(cudaMemsetAsync(w->v, 0, n * sizeof(double), s), err);
+    B200_CUDA_E(cudaMemsetAsync(w->p, 0, n * sizeof(double), s), err);
+    k_begin<<<1, 1, 0, s>>>(w->sc);
+    count_launch();
+    // ---- inner loop: batches of iterations, double-buffered status polling
+    int batch = 4;
+    int cur = 0;
+    auto enqueue_batch = [&](int slot) -> int {
+      for (int i = 0; i < batch; ++i) enqueue_iteration(m, b, x);
+      B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+      B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
+      return 0;
+    };
+    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
+    KrylovScalars done{};
+    for (;;) {
+      batch = std::min(batch * 2, 32);
+      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
+      B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
+      if (H[1 + cur].status != KS_RUNNING) break;
+      cur ^= 1;
+    }
+    B200_CUDA_E(cudaStreamSynchronize(s), err);  // drain the no-op batch
+    done = H[1 + (cur ^ 1)];                     // latest snapshot (status is sticky)
+    it = done.it;
+    mv = done.mv;
+    B200_CUDA_E(cudaGetLastError(), err);
+    if (done.status == KS_BREAKDOWN) {
+      // shadow residual went orthogonal: restart from the explicit residual unless the
+      // previous restart made no progress (solvers.py:144-157)
+      if (last_bd >= 0.0 && done.res >= 0.999 * last_bd) {
+        if (info) *info = b200fem_solve_info{it, mv, restarts, done.res, tol};
+        if (err) {
+          err->iterations = it;
+          err->value = done.res;
+        }
+        set_err(err, B200FEM_E_BREAKDOWN, "BiCGSTAB breakdown without progress at iteration %lld (residual %.3e)",
+                it, done.res);
+        return B200FEM_E_BREAKDOWN;
+      }
+      last_bd = done.res;
+    }
+    // KS_CONV_INNER / KS_MAXED / restart: back to the explicit residual check
+  }
+}
+
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" {
+
+int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *data) {
+  Ctx *c = (Ctx *)ctx;
+  if (!out || !c) return B200FEM_E_INVALID;
+  Matrix *m = new Matrix();
+  m->n = c->n_dofs;
+  m->nnz = c->nnz;
+  m->data = data;
+  m->stream = c->stream;
+  m->diag_slots = c->diag;
+  if (c->vec == 3) {
+    m->kind = MK_FEM3;
+    m->nbr_ptr = c->nbr_ptr;
+    m->nbr = c->nbr;
+    m->indptr = c->indptr;
+  } else {
+    m->kind = MK_CSR;
+    m->indptr = c->indptr;
+    m->indices = c->nbr;  // vec 1: node list == column list
+    m->lanes = 8;
+  }
+  *out = (b200fem_matrix *)m;
+  return 0;
+}
+
+int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr, const int32_t *indices,
+                       const double *data, void *stream) {
+  if (!out || n < 0 || nnz < 0) return B200FEM_E_INVALID;
+  Matrix *m = new Matrix();
+  m->kind = MK_CSR;
+  m->n = n;
+  m->nnz = nnz;
+  m->indptr = indptr;
+  m->indices = indices;
+  m->data = data;
+  m->stream = (cudaStream_t)stream;
+  const double avg = n ? (double)nnz / (double)n : 0.0;
+  m->lanes = avg <= 6 ? 4 : (avg <= 24 ? 8 : (avg <= 64 ? 16 : 32));
+  *out = (b200fem_matrix *)m;
+  return 0;
+}
+
+int b200fem_matrix_set_data(b200fem_matrix *mm, const double *data) {
+  ((Matrix *)mm)->data = data;
+  return 0;
+}
+
+int b200fem_matrix_destroy(b200fem_matrix *mm) {
+  Matrix *m = (Matrix *)mm;
+  if (!m) return 0;
+  cudaStreamSynchronize(m->stream);
+  free_work(m->kw);
+  delete m;
+  return 0;
+}
+
+int b200fem_matvec(b200fem_matrix *mm, const double *x, double *y) {
+  Matrix *m = (Matrix *)mm;
+  if (m->n == 0) return 0;
+  SpmvArgs a{x, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  return launch_spmv(m, SP_PLAIN, a, nullptr);
+}
+
+int b200fem_diagonal(b200fem_matrix *mm, double *diag) {
+  Matrix *m = (Matrix *)mm;
+  if (m->n == 0) return 0;
+  int st = ensure_work(m);
+  if (st) return st;
+  st = launch_diagonal(m, diag, m->kw->inv, &m->kw->red, nullptr);
+  return st;
+}
+
+int b200fem_bicgstab(b200fem_matrix *mm, const double *b, double *x, int32_t has_x0, double rel_tol, double abs_tol,
+                     int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+  Matrix *m = (Matrix *)mm;
+  if (m->n == 0) {
+    if (info) memset(info, 0, sizeof(*info));
+    return 0;
+  }
+  return bicgstab(m, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference goldens and the oracle.
+
+Bars (north_star): integer maps bit-exact; FP64 residuals / solutions to relative L2 <= 1e-8
+(tighter where the arithmetic allows: R and K at a fixed U to 1e-12).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2212_00964_b200 as fem
+from cases import CASES, schedule_factors
+from conftest import load_golden
+from oracle_cases import build_oracle
+from pkg_cases import build, locator
+
+pytestmark = pytest.mark.gpu
+ALL = list(CASES)
+STATIC = [n for n in ALL if "schedule" not in CASES[n]]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_pattern_and_maps_bit_exact(name):
+    g = load_golden(name)
+    mesh, prob, _ = build(name)
+    assert np.array_equal(mesh.nodes, g["nodes"]) and np.array_equal(mesh.cells, g["cells"])
+    ws = fem.workspace(prob)
+    assert np.array_equal(ws.indptr, g["indptr"])
+    assert np.array_equal(ws.indices, g["indices"])
+    assert np.array_equal(ws.dest, g["dest"])
+    assert np.array_equal(ws.diag_slots, g["diag_slots"])
+    assert np.array_equal(ws.dir_dofs, g["dir_dofs"]) and np.array_equal(ws.dir_values, g["dir_values"])
+    assert np.array_equal(ws.dir_row_slots, g["dir_row_slots"])
+    assert np.allclose(ws.f_neumann, g["f_neumann"], rtol=1e-13, atol=1e-15)
+    assert np.allclose(ws.f_body, g["f_body"], rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_residual_and_jacobian_match_reference(name):
+    g = load_golden(name)
+    _, prob, U = build(name)
+    if "state_eps" in g:
+        prob.state = fem.QuadPointState(g["state_eps"], g["state_sig"])
+        U = g["U_test"]
+    R = fem.assemble_residual(prob, U)
+    assert rel(R, g["R_test"]) < 1e-12
+    if "R_test_nodir" in g:
+        assert rel(fem.assemble_residual(prob, U, apply_dirichlet=False), g["R_test_nodir"]) < 1e-12
+    K = fem.assemble_jacobian(prob, U)
+    assert np.array_equal(K.indptr, g["indptr"]) and np.array_equal(K.indices, g["indices"])
+    assert rel(K.data, g["K_test"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", STATIC)
+def test_newton_solution_matches_reference(name):
+    g = load_golden(name)
+    _, prob, _ = build(name)
+    U, rep = fem.newton_solve(prob, cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11),
+                              lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14))
+    assert rel(U, g["U_tight"]) < 1e-8
+    assert rep.converged
+    _, prob2, _ = build(name)
+    Ud, rep2 = fem.newton_solve(prob2, cfg=fem.NewtonConfig(**CASES[name].get("newton", {})))
+    assert rep2.n_iterations == len(g["norms_default"]) - 1
+    assert rel(Ud, g["U_default"]) < 1e-6
+    assert np.allclose(fem.volume_averaged_stress(prob, U), g["avg_stress"], rtol=1e-8, atol=1e-8)
+
+
+def test_c1_known_answers():
+    """SURVEY Appendix B / BASELINE config 1 on the GPU."""
+    g = load_golden("c1")
+    _, prob, _ = build("c1")
+    hist = fem.incremental_solve(prob, fem.LoadSchedule.ramp(1), reaction_locator=locator(("plane", 0, 0.0)))
+    rec = hist.steps[0]
+    assert rec.newton_iterations == 1
+    assert abs(rec.residual_history[0] - 3.5) < 1e-12
+    assert abs(np.linalg.norm(rec.U) - 0.3231822390393) < 1e-9
+    assert abs(rec.reaction - 16.0) < 1e-6
+    assert rel(rec.U, g["U_default"]) < 1e-8
+
+
+def test_nh_criterion6_history():
+    """pkg/test_output.txt:213 history reproduced on the GPU (first three norms to 1e-9)."""
+    _, prob, _ = build("nh_crit6")
+    _, rep = fem.newton_solve(prob, cfg=fem.NewtonConfig(rel_tol=1e-9, abs_tol=1e-10))
+    pub = [0.060000000000000005, 7.457066921927957, 0.0012056401689689693, 3.471924728500236e-11]
+    assert len(rep.residual_norms) == 4
+    assert np.allclose(rep.residual_norms[:3], pub[:3], rtol=1e-9)
+    assert rep.residual_norms[3] < 1e-9
+    n = np.array(rep.residual_norms)
+    below = n[(n < 1.0) & (n > 1e-13)]
+    assert np.log(below[-1]) / np.log(below[-2]) >= 1.5
+
+
+@pytest.mark.parametrize("name", ["j2_block", "j2_8"])
+def test_j2_incremental_matches_reference(name):
+    g = load_golden(name)
+    _, prob, _ = build(name)
+    loc, comp = CASES[name]["reaction"]
+    hist = fem.incremental_solve(prob, fem.LoadSchedule(tuple(schedule_factors(CASES[name]["schedule"]))),
+                                 cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-12),
+                                 lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14),
+                                 reaction_locator=locator(loc), reaction_component=comp)
+    react = np.array([r.reaction for r in hist.steps])
+    assert np.allclose(react, g["reactions"], rtol=1e-8, atol=1e-7)
+    assert rel(hist.steps[-1].U, g["U_final"]) < 1e-8
+    assert np.allclose(np.array([r.avg_stress for r in hist.steps]), g["avg_stress_hist"], rtol=1e-8, atol=1e-6)
+
+
+def test_j2_scalar_oracle_hysteresis():
+    """Reference tests/test_solvers.py:199-228: single cell, affine ramp-and-back vs a scalar return map."""
+    mesh = fem.generate_box_mesh(1, 1, 1, 1, 1, 1)
+    alu = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+    E0 = np.diag([0.0, 0.0, 0.012])
+    specs = [fem.DirichletSpec(fem.BoundaryLocator.everywhere(), c,
+                               (lambda c: lambda p: (np.atleast_2d(p) @ E0.T)[..., c])(c)) for c in range(3)]
+    prob = fem.J2PlasticityProblem(mesh, alu, specs)
+    sched = fem.LoadSchedule.ramp_and_back(10)
+    hist = fem.incremental_solve(prob, sched)
+    dev0 = E0 - np.trace(E0) / 3.0 * np.eye(3)
+    mag = np.sqrt(1.5 * (dev0 * dev0).sum())
+    cd = press = ap = 0.0
+    for rec, a in zip(hist.steps, sched.factors):
+        da = a - ap
+        ct = cd + 2.0 * alu.mu * da
+        se = abs(ct) * mag
+        cd = ct if se <= alu.sigma_yield else ct * alu.sigma_yield / se
+        press += (alu.lam + 2.0 * alu.mu / 3.0) * np.trace(E0) * da
+        ap = a
+        sig = cd * dev0 + press * np.eye(3)
+        assert np.abs(rec.avg_stress - sig).max() < 1e-10 * max(1.0, np.abs(sig).max())
+    assert abs(hist.steps[-1].avg_stress[2, 2]) > 1.0
+
+
+@pytest.mark.parametrize("name", ["c1", "nh_block", "poisson", "simp"])
+def test_spmv_matches_oracle(name, rng):
+    _, prob, U = build(name)
+    K = fem.assemble_jacobian(prob, U)
+    x = rng.standard_normal(prob.n_dofs)
+    y = K @ x
+    y_ref = orc.csr_matvec(K.indptr, K.indices, K.data, x, use_numba=False)
+    assert rel(y, y_ref) < 1e-14
+    # generic CSR path (host-built matrix) on the same operator
+    K2 = fem.CsrMatrix(K.indptr, K.indices, K.data)
+    assert rel(K2 @ x, y_ref) < 1e-14
+    assert np.array_equal(K.diagonal(), orc._diag_of(K.indptr, K.indices, K.data))
+
+
+def test_determinism_bitwise(rng):
+    _, prob, U = build("nh_block")
+    R1 = fem.assemble_residual(prob, U)
+    R2 = fem.assemble_residual(prob, U)
+    K1 = fem.assemble_jacobian(prob, U).data
+    K2 = fem.assemble_jacobian(prob, U).data
+    assert np.array_equal(R1, R2) and np.array_equal(K1, K2)
+    U1, _ = fem.newton_solve(prob)
+    U2, _ = fem.newton_solve(prob)
+    assert np.array_equal(U1, U2)
+
+
+def test_oracle_agreement_random_states(rng):
+    """Larger-than-golden meshes: the GPU path vs the oracle at the same seeded inputs."""
+    for name in ("nh_block", "simp_nh", "poisson_design"):
+        case = dict(CASES[name])
+        case["dims"] = tuple(2 * d for d in case["dims"])
+        _, prob, U = build(name, case)
+        po, _ = build_oracle(name, case)
+        if prob.theta is not None:
+            po_theta = prob.theta
+            if po.simp_theta is not None:
+                po.simp_theta = po_theta
+            if po.source_theta is not None:
+                po.source_theta = po_theta
+        assert rel(fem.assemble_residual(prob, U), orc.residual(po, U)) < 1e-12
+        assert rel(fem.assemble_jacobian(prob, U).data, orc.jacobian(po, U)) < 1e-12
+
+
+# ----------------------------------------------- reference tests/test_solvers.py
+def _dense_csr(A):
+    n = A.shape[0]
+    ip, ix, dt = [0], [], []
+    for i in range(n):
+        c = np.flatnonzero(A[i])
+        ix.extend(c)
+        dt.extend(A[i, c])
+        ip.append(len(ix))
+    return fem.CsrMatrix(np.array(ip, np.int32), np.array(ix, np.int32), np.array(dt))
+
+
+def test_bicgstab_identity_diagonal_zero(rng):
+    b = rng.standard_normal(17)
+    assert np.allclose(fem.bicgstab_jacobi(_dense_csr(np.eye(17)), b), b, rtol=1e-12)
+    d = rng.uniform(0.5, 4.0, 23)
+    b = rng.standard_normal(23)
+    assert np.allclose(fem.bicgstab_jacobi(_dense_csr(np.diag(d)), b), b / d, rtol=1e-10)
+    assert np.array_equal(fem.bicgstab_jacobi(_dense_csr(np.diag(np.full(5, 2.0))), np.zeros(5)), np.zeros(5))
+
+
+def _poisson_matrix(n):
+    mesh = fem.generate_box_mesh(n, n, n, 1, 1, 1)
+    onb = locator(("onbox", 1.0, 1.0, 1.0))
+    prob = fem.PoissonProblem(mesh, 1.0, [fem.DirichletSpec(onb, 0, lambda p: 0.0)])
+    return prob, fem.assemble_jacobian(prob, np.zeros(prob.n_dofs))
+
+
+def test_bicgstab_matches_dense_lu(rng):
+    prob, A = _poisson_matrix(4)
+    b = rng.standard_normal(prob.n_dofs)
+    x = fem.bicgstab_jacobi(A, b, cfg=fem.LinearSolveConfig(rel_tol=1e-12, abs_tol=1e-14))
+    x_lu = np.linalg.solve(A.todense(), b)
+    assert np.abs(x - x_lu).max() / np.abs(x_lu).max() < 1e-8
+
+
+def test_bicgstab_residual_bound_and_nonconvergence(rng):
+    prob, A = _poisson_matrix(3)
+    b = rng.standard_normal(prob.n_dofs)
+    cfg = fem.LinearSolveConfig(rel_tol=1e-9, abs_tol=1e-12)
+    x = fem.bicgstab_jacobi(A, b, cfg=cfg)
+    assert np.linalg.norm(A.todense() @ x - b) <= max(cfg.rel_tol * np.linalg.norm(b), cfg.abs_tol)
+    with pytest.raises(fem.LinearSolverError) as err:
+        fem.bicgstab_jacobi(A, b, cfg=fem.LinearSolveConfig(rel_tol=1e-14, abs_tol=1e-16, max_iters=2))
+    assert err.value.residual is not None and err.value.iterations == 2
+
+
+def test_zero_diagonal_rejected():
+    A = fem.CsrMatrix(np.array([0, 1, 2], np.int32), np.array([1, 0], np.int32), np.array([1.0, 1.0]))
+    with pytest.raises(fem.LinearSolverError, match="zero diagonal"):
+        fem.bicgstab_jacobi(A, np.ones(2))
+
+
+def test_inverted_deformation_names_element():
+    """Reference tests/test_assembly.py:390-400."""
+    mesh = fem.generate_box_mesh(2, 1, 1, 2, 1, 1)
+    prob = fem.NeoHookeanProblem(mesh, fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0), [])
+    U = np.zeros(prob.n_dofs)
+    ed = fem.workspace(prob).edofs
+    only1 = np.setdiff1d(ed[1], ed[0])
+    U[only1[::3]] = -1.5
+    with pytest.raises(fem.InvertedDeformationError, match="element 1"):
+        fem.assemble_residual(prob, U)
+    with pytest.raises(fem.InvertedDeformationError, match="element 1"):
+        fem.assemble_jacobian(prob, U)
+
+
+def test_inverted_element_rejected():
+    nodes, cells = orc.box_mesh(1, 1, 1, 1, 1, 1)
+    cells = cells[:, [1, 0, 3, 2, 5, 4, 7, 6]]  # mirrored -> det J < 0
+    mesh = fem.Mesh(nodes, cells)
+    prob = fem.LinearElasticityProblem(mesh, fem.ElasticConstants(E=1.0, nu=0.25), [])
+    with pytest.raises(fem.InvertedElementError, match="non-positive Jacobian"):
+        fem.assemble_residual(prob, np.zeros(prob.n_dofs))
+
+
+def test_all_dirichlet_identity_and_newton():
+    mesh = fem.generate_box_mesh(1, 1, 1, 1, 1, 1)
+    A = np.diag([0.01, -0.005, 0.02])
+    specs = [fem.DirichletSpec(fem.BoundaryLocator.everywhere(), c,
+                               (lambda c: lambda p: (np.atleast_2d(p) @ A.T)[..., c])(c)) for c in range(3)]
+    prob = fem.LinearElasticityProblem(mesh, fem.ElasticConstants(E=70e3, nu=0.3), specs)
+    K = fem.assemble_jacobian(prob, np.zeros(prob.n_dofs)).todense()
+    assert np.array_equal(K, np.eye(prob.n_dofs))
+    U, rep = fem.newton_solve(prob)
+    assert rep.n_iterations == 1
+    assert np.allclose(U, (mesh.nodes @ A.T).ravel(), atol=1e-14)
+
+
+@pytest.mark.parametrize("dims", [(3, 3, 3), (4, 2, 2)])
+@pytest.mark.parametrize("kind", ["le", "nh", "j2"])
+def test_patch_affine_reproduction(kind, dims):
+    """Reference tests/test_solvers.py:148-161 and acceptance criterion 5."""
+    from cases import PATCH_A
+    mesh = fem.generate_box_mesh(*dims, 1, 1, 1)
+    onb = locator(("onbox", 1.0, 1.0, 1.0))
+    specs = [fem.DirichletSpec(onb, c, (lambda c: lambda p: (np.atleast_2d(p) @ PATCH_A.T)[..., c])(c))
+             for c in range(3)]
+    alu = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+    cls = {"le": fem.LinearElasticityProblem, "nh": fem.NeoHookeanProblem, "j2": fem.J2PlasticityProblem}[kind]
+    U, _ = fem.newton_solve(cls(mesh, alu, specs))
+    assert np.abs(U - (mesh.nodes @ PATCH_A.T).ravel()).max() < 1e-10
+
+
+def test_newton_nonconvergence_and_incremental_abort():
+    alu = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+    mesh = fem.generate_box_mesh(2, 2, 2, 1, 1, 1)
+    fixed = [fem.DirichletSpec(fem.BoundaryLocator.plane(2, 0.0), c, lambda p: 0.0) for c in range(3)]
+    prob = fem.NeoHookeanProblem(mesh, alu, fixed + [fem.DirichletSpec(fem.BoundaryLocator.plane(2, 1.0), 2,
+                                                                        lambda p: 0.02)])
+    with pytest.raises(fem.NonConvergenceError) as err:
+        fem.newton_solve(prob, cfg=fem.NewtonConfig(rel_tol=1e-16, abs_tol=1e-18, max_iters=3))
+    assert len(err.value.residual_norms) == 4
+    prob2 = fem.NeoHookeanProblem(mesh, alu, fixed + [fem.DirichletSpec(fem.BoundaryLocator.plane(2, 1.0), 2,
+                                                                         lambda p: 0.4)])
+    with pytest.raises(fem.NonConvergenceError, match="load step"):
+        fem.incremental_solve(prob2, fem.LoadSchedule((1.0,)), cfg=fem.NewtonConfig(max_iters=2))
+
+
+def test_reaction_force_equilibrium():
+    """Reference tests/test_solvers.py:231-245."""
+    mesh = fem.generate_box_mesh(3, 3, 3, 1, 1, 1)
+    alu = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+    A = np.diag([0.0, 0.0, 0.01])
+    onb = locator(("onbox", 1.0, 1.0, 1.0))
+    specs = [fem.DirichletSpec(onb, c, (lambda c: lambda p: (np.atleast_2d(p) @ A.T)[..., c])(c)) for c in range(3)]
+    prob = fem.LinearElasticityProblem(mesh, alu, specs)
+    top, bot = fem.BoundaryLocator.plane(2, 1.0), fem.BoundaryLocator.plane(2, 0.0)
+    assert fem.reaction_force(prob, np.zeros(prob.n_dofs), top, 2) == 0.0
+    U, _ = fem.newton_solve(prob)
+    szz = alu.lam * 0.01 + 2 * alu.mu * 0.01
+    rt, rb = fem.reaction_force(prob, U, top, 2), fem.reaction_force(prob, U, bot, 2)
+    assert abs(rt - szz) < 1e-10 * abs(szz)
+    assert abs(rt + rb) < 1e-9 * abs(rt)
+
+
+def test_quad_point_stress_matches_oracle(rng):
+    _, prob, U = build("simp_nh")
+    po, _ = build_oracle("simp_nh")
+    po.simp_theta = prob.theta
+    s = fem.quad_point_stress(prob, U)
+    assert s.shape == (prob.mesh.n_cells, 8, 3, 3)
+    assert rel(s, orc.qp_flux(po, U)) < 1e-12
+
+
+def test_device_tensors_stay_on_device():
+    import torch
+    _, prob, U = build("nh_block")
+    Ud = torch.tensor(U, device="cuda")
+    R = fem.assemble_residual(prob, Ud)
+    assert isinstance(R, torch.Tensor) and R.is_cuda
+    Us, rep = fem.newton_solve(prob, Ud)
+    assert isinstance(Us, torch.Tensor) and Us.is_cuda and rep.converged
