@@ -132,6 +132,10 @@ struct Matrix {
   cudaStream_t stream = nullptr;
   int lanes = 8;  // CSR sub-warp width
   KrylovWork *kw = nullptr;
+  // FEM3 bulk-copy pipeline: node chunks [chunk_node[c], chunk_node[c+1]) sized to a stage
+  int32_t *chunk_node = nullptr;
+  int n_chunks = 0;
+  bool use_tma = false;
 };
 
 // allocation helpers
@@ -163,6 +167,7 @@ struct SpmvArgs {
 };
 int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
+int prepare_fem3_chunks(Matrix *m);
 
 // element kernels
 int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int apply_dirichlet,
@@ -187,8 +192,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Deterministic block reduction of NV values per thread; result valid in thread 0.
-template <int NV>
-__device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sh)[kWarps]) {
+template <int NV, int NW = kWarps>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sh)[NW]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
@@ -201,7 +206,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sh)[kWarp
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       double a = 0.0;
-      for (int k = 0; k < kWarps; ++k) a += sh[j][k];
+      for (int k = 0; k < NW; ++k) a += sh[j][k];
       v[j] = a;
     }
   }
@@ -209,12 +214,12 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], double (*sh)[kWarp
 
 // Write this block's partials; return true in ALL threads of the last block to finish,
 // which then holds the fully reduced values in `tot` (thread 0 valid).
-template <int NV>
+template <int NV, int NW = kWarps>
 __device__ __forceinline__ bool block_partials_and_finish(double (&v)[NV], RedScratch red,
                                                           double (&tot)[NV]) {
-  __shared__ double sh[NV][kWarps];
+  __shared__ double sh[NV][NW];
   __shared__ bool last;
-  block_reduce<NV>(v, sh);
+  block_reduce<NV, NW>(v, sh);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) red.partials[j * kRedBlocks + blockIdx.x] = v[j];
@@ -234,7 +239,7 @@ __device__ __forceinline__ bool block_partials_and_finish(double (&v)[NV], RedSc
     acc[j] = a;
   }
   __syncthreads();
-  block_reduce<NV>(acc, sh);
+  block_reduce<NV, NW>(acc, sh);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {

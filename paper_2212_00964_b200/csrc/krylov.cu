@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -267,6 +268,15 @@ int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *dat
     m->nbr_ptr = c->nbr_ptr;
     m->nbr = c->nbr;
     m->indptr = c->indptr;
+    // Bulk-copy pipelined SpMV is opt-in: measured 4.58 TB/s vs 5.36 TB/s for the register-
+    // streaming kernel on config 3 (profiles/r01_spmv_variants.md).
+    if (getenv("B200FEM_SPMV_TMA")) {
+      int st = prepare_fem3_chunks(m);
+      if (st) {
+        delete m;
+        return st;
+      }
+    }
   } else {
     m->kind = MK_CSR;
     m->indptr = c->indptr;
@@ -304,6 +314,7 @@ int b200fem_matrix_destroy(b200fem_matrix *mm) {
   if (!m) return 0;
   cudaStreamSynchronize(m->stream);
   free_work(m->kw);
+  cudaFree(m->chunk_node);
   delete m;
   return 0;
 }

@@ -16,30 +16,56 @@
 // explicit residual r = D^-1 (b - A x) with ||D r||^2 and ||r||^2 (solvers.py:115-116).
 // Reductions use a fixed grid and a last-block finish -> deterministic.
 
+#include <algorithm>
+#include <vector>
+
 #include "internal.cuh"
 
 namespace b200 {
 
+// Row operands the epilogue needs, loaded at the START of a row's work so their latency
+// overlaps the value stream instead of serialising after the reduction.
+struct RowPre {
+  double inv, aux, dg, xi;
+};
+
+template <int MODE>
+__device__ __forceinline__ RowPre spmv_preload(int64_t i, const SpmvArgs &a) {
+  RowPre p{0.0, 0.0, 0.0, 0.0};
+  if (MODE == SP_JACOBI_R0) {
+    p.inv = __ldg(a.inv + i);
+    p.aux = __ldg(a.aux + i);
+  } else if (MODE == SP_JACOBI_TT) {
+    p.inv = __ldg(a.inv + i);
+    p.xi = __ldg(a.x + i);
+  } else if (MODE == SP_RESIDUAL) {
+    p.inv = __ldg(a.inv + i);
+    p.aux = __ldg(a.aux + i);
+    p.dg = __ldg(a.dg + i);
+  }
+  return p;
+}
+
 // Post-process row i's dot-product value `acc` for the mode; accumulate reduction terms.
 template <int MODE>
-__device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvArgs &a, double &red0,
-                                              double &red1) {
+__device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvArgs &a, const RowPre &p,
+                                              double &red0, double &red1) {
   if (MODE == SP_PLAIN) {
     a.y[i] = acc;
   } else if (MODE == SP_JACOBI_R0) {
-    const double v = a.inv[i] * acc;
+    const double v = p.inv * acc;
     a.y[i] = v;
-    red0 = fma(a.aux[i], v, red0);
+    red0 = fma(p.aux, v, red0);
   } else if (MODE == SP_JACOBI_TT) {
-    const double t = a.inv[i] * acc;
+    const double t = p.inv * acc;
     a.y[i] = t;
     red0 = fma(t, t, red0);
-    red1 = fma(t, a.x[i], red1);
+    red1 = fma(t, p.xi, red1);
   } else {  // SP_RESIDUAL
-    const double r = a.inv[i] * (a.aux[i] - acc);
+    const double r = p.inv * (p.aux - acc);
     a.y[i] = r;
     a.aux2[i] = r;
-    const double dr = a.dg[i] * r;
+    const double dr = p.dg * r;
     red0 = fma(dr, dr, red0);
     red1 = fma(r, r, red1);
   }
@@ -66,8 +92,30 @@ __device__ __forceinline__ void spmv_stage(KrylovScalars *S, const double (&tot)
   }
 }
 
+// Sum three per-lane partials over the warp with a reduce-scatter (6 double shuffles
+// instead of 3 full butterflies = 15): afterwards lane 0 holds row 0, lane 8 row 1,
+// lane 16 row 2.  Fixed tree -> deterministic.
+__device__ __forceinline__ double warp_sum3(double y0, double y1, double y2, int lane) {
+  const bool h4 = lane & 16;
+  const double s0 = h4 ? y0 : y2, s1 = h4 ? y1 : 0.0;
+  double k0 = (h4 ? y2 : y0) + __shfl_xor_sync(0xffffffffu, s0, 16);
+  double k1 = (h4 ? 0.0 : y1) + __shfl_xor_sync(0xffffffffu, s1, 16);
+  const bool h3 = lane & 8;
+  double kk = (h3 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+  return kk;
+}
+
+// Warp per node, lane per neighbour node j: the lane loads x_m (3 doubles, L2-resident)
+// once and the 3x3 block of values A[3n+c, 3m+k] from the three contiguous row segments
+// (rows are 3*cnt long; lane j's entries sit at 3j..3j+2 of each row, so a warp load
+// instruction covers one row's 27*24 B contiguous span).  12 independent loads per lane,
+// ~60 warp instructions per node; values are streamed with an evict-first hint so x stays
+// in L2; the 3 row sums use a 6-shuffle reduce-scatter.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_spmv_fem3(const int32_t *__restrict__ nbr_ptr,
+__global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__restrict__ nbr_ptr,
                                                         const int32_t *__restrict__ nbr,
                                                         const double *__restrict__ data, int64_t n_nodes,
                                                         SpmvArgs a, RedScratch red) {
@@ -78,53 +126,229 @@ __global__ void __launch_bounds__(kThreads) k_spmv_fem3(const int32_t *__restric
   const double *__restrict__ x = a.x;
   double red0 = 0.0, red1 = 0.0;
   for (int64_t n = warp0; n < n_nodes; n += nwarps) {
-    const int p0 = nbr_ptr[n];
-    const int cnt = nbr_ptr[n + 1] - p0;
+    const int p0 = __ldg(nbr_ptr + n);
+    const int cnt = __ldg(nbr_ptr + n + 1) - p0;
     const int L = 3 * cnt;
     const double *__restrict__ blk = data + 9 * (int64_t)p0;
+    const bool row_lane = (lane & 7) == 0 && lane < 24;
+    const int64_t row = 3 * n + (lane >> 3);
+    RowPre pre{0.0, 0.0, 0.0, 0.0};
+    if (row_lane) pre = spmv_preload<MODE>(row, a);
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    if (cnt <= 32) {
-      const int mine = lane < cnt ? nbr[p0 + lane] : 0;
-      for (int e0 = 0; e0 < 3 * L; e0 += 32) {  // warp-uniform trip count: shuffles see all lanes
-        const int e = e0 + lane;
-        const bool ok = e < 3 * L;
-        const int c = (e >= L) + (e >= 2 * L);
-        const int r = e - c * L;
-        const int j = ok ? r / 3 : 0;
-        const int k = r - 3 * j;
-        const int m = __shfl_sync(0xffffffffu, mine, j);
-        if (ok) {
-          const double prod = __ldg(blk + e) * __ldg(x + 3 * (int64_t)m + k);
-          if (c == 0) y0 += prod;
-          else if (c == 1) y1 += prod;
-          else y2 += prod;
-        }
-      }
-    } else {
-      for (int e = lane; e < 3 * L; e += 32) {
-        const int c = (e >= L) + (e >= 2 * L);
-        const int r = e - c * L;
-        const int j = r / 3;
-        const int k = r - 3 * j;
-        const int m = nbr[p0 + j];
-        const double prod = __ldg(blk + e) * __ldg(x + 3 * (int64_t)m + k);
-        if (c == 0) y0 += prod;
-        else if (c == 1) y1 += prod;
-        else y2 += prod;
+    for (int j = lane; j < cnt; j += 32) {
+      const int m = __ldg(nbr + p0 + j);
+      const double *__restrict__ xm = x + 3 * (int64_t)m;
+      const double *__restrict__ r0 = blk + 3 * j;
+      const double a00 = __ldcs(r0), a01 = __ldcs(r0 + 1), a02 = __ldcs(r0 + 2);
+      const double a10 = __ldcs(r0 + L), a11 = __ldcs(r0 + L + 1), a12 = __ldcs(r0 + L + 2);
+      const double a20 = __ldcs(r0 + 2 * L), a21 = __ldcs(r0 + 2 * L + 1), a22 = __ldcs(r0 + 2 * L + 2);
+      const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+      y0 = fma(a02, x2, fma(a01, x1, fma(a00, x0, y0)));
+      y1 = fma(a12, x2, fma(a11, x1, fma(a10, x0, y1)));
+      y2 = fma(a22, x2, fma(a21, x1, fma(a20, x0, y2)));
+    }
+    const double acc = warp_sum3(y0, y1, y2, lane);
+    if (row_lane) spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2>(v2, red, tot) && threadIdx.x == 0) spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// FEM3 SpMV, Blackwell bulk-copy pipeline.  One persistent CTA per SM: a producer lane
+// streams contiguous node chunks (their CSR values and neighbour lists, which are
+// contiguous in memory for consecutive nodes) into a 4-stage shared-memory ring with
+// cp.async.bulk + mbarrier complete_tx; 16 consumer warps compute the node rows from
+// shared memory and gather x from L2.  The copy engine keeps ~150 KB per SM in flight
+// without spending registers, which is what the register-limited LDG kernel above
+// cannot do.  Same arithmetic and summation order as k_spmv_fem3 -> bit-identical y.
+constexpr int kTmaConsumers = 16;
+constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
+constexpr int kTmaStages = 4;
+constexpr int kTmaValBytes = 44 * 1024;
+constexpr int kTmaNbrBytes = 2560;
+constexpr int kTmaStageBytes = kTmaValBytes + kTmaNbrBytes;
+constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// One node's three row sums from a value block `sv` (stage or global) and its neighbour ids.
+__device__ __forceinline__ void node_rows(const double *sv, const int32_t *sn, int cnt, const double *__restrict__ x,
+                                          int lane, double &y0, double &y1, double &y2) {
+  const int L = 3 * cnt;
+  for (int j = lane; j < cnt; j += 32) {
+    const int m = sn[j];
+    const double *__restrict__ xm = x + 3 * (int64_t)m;
+    const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+    const double *r0 = sv + 3 * j;
+    y0 = fma(r0[2], x2, fma(r0[1], x1, fma(r0[0], x0, y0)));
+    y1 = fma(r0[L + 2], x2, fma(r0[L + 1], x1, fma(r0[L], x0, y1)));
+    y2 = fma(r0[2 * L + 2], x2, fma(r0[2 * L + 1], x1, fma(r0[2 * L], x0, y2)));
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t *__restrict__ nbr_ptr,
+                                                                 const int32_t *__restrict__ nbr,
+                                                                 const double *__restrict__ data,
+                                                                 const int32_t *__restrict__ chunk_node, int n_chunks,
+                                                                 int64_t total_blocks, SpmvArgs a, RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t *empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // the last chunk's end may not be 16-byte aligned: it is read from global memory instead
+  const uint64_t val_end = (uint64_t)total_blocks * 72, nbr_end = (uint64_t)total_blocks * 4;
+  double red0 = 0.0, red1 = 0.0;
+  if (warp == kTmaConsumers) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int s = it % kTmaStages;
+        const uint32_t ph = (it / kTmaStages) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        const int64_t p0 = __ldg(nbr_ptr + __ldg(chunk_node + c)), p1 = __ldg(nbr_ptr + __ldg(chunk_node + c + 1));
+        const uint64_t vb0 = (72ull * p0) & ~15ull, vb1 = std::min((72ull * p1 + 15) & ~15ull, val_end & ~15ull);
+        const uint64_t nb0 = (4ull * p0) & ~15ull, nb1 = std::min((4ull * p1 + 15) & ~15ull, nbr_end & ~15ull);
+        mbar_expect_tx(full + s, (uint32_t)((vb1 - vb0) + (nb1 - nb0)));
+        uint8_t *stage = smem + s * kTmaStageBytes;
+        if (vb1 > vb0) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(data) + vb0, (uint32_t)(vb1 - vb0), full + s);
+        if (nb1 > nb0)
+          bulk_g2s(stage + kTmaValBytes, reinterpret_cast<const uint8_t *>(nbr) + nb0, (uint32_t)(nb1 - nb0), full + s);
       }
     }
-    y0 = warp_sum(y0);
-    y1 = warp_sum(y1);
-    y2 = warp_sum(y2);
-    if (lane < 3) {
-      const double acc = lane == 0 ? y0 : (lane == 1 ? y1 : y2);
-      spmv_epilogue<MODE>(3 * n + lane, acc, a, red0, red1);
+    __syncwarp();  // reconverge the producer warp before the block-wide reduction barrier
+  } else {
+    int it = 0;
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+      const int s = it % kTmaStages;
+      const uint32_t ph = (it / kTmaStages) & 1;
+      const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
+      const int64_t pc = __ldg(nbr_ptr + n0), pe = __ldg(nbr_ptr + n1);
+      const uint64_t vb0 = (72ull * pc) & ~15ull, nb0 = (4ull * pc) & ~15ull;
+      const bool tail = (72ull * pe > (val_end & ~15ull)) || (4ull * pe > (nbr_end & ~15ull));
+      const uint8_t *stage = smem + s * kTmaStageBytes;
+      // prefetch this warp's node bounds and epilogue operands while the stage lands
+      int nA = n0 + warp, nB = n0 + warp + kTmaConsumers;
+      int64_t pA = 0, pB = 0;
+      int cA = 0, cB = 0;
+      if (nA < n1) {
+        pA = __ldg(nbr_ptr + nA);
+        cA = __ldg(nbr_ptr + nA + 1) - (int)pA;
+      }
+      if (nB < n1) {
+        pB = __ldg(nbr_ptr + nB);
+        cB = __ldg(nbr_ptr + nB + 1) - (int)pB;
+      }
+      const bool row_lane = (lane & 7) == 0 && lane < 24;
+      RowPre preA{0.0, 0.0, 0.0, 0.0}, preB{0.0, 0.0, 0.0, 0.0};
+      if (row_lane && nA < n1) preA = spmv_preload<MODE>(3 * (int64_t)nA + (lane >> 3), a);
+      if (row_lane && nB < n1) preB = spmv_preload<MODE>(3 * (int64_t)nB + (lane >> 3), a);
+      mbar_wait(full + s, ph);
+      double yA0 = 0.0, yA1 = 0.0, yA2 = 0.0, yB0 = 0.0, yB1 = 0.0, yB2 = 0.0;
+      if (!tail) {
+        if (nA < n1)
+          node_rows(reinterpret_cast<const double *>(stage + (72ull * pA - vb0)),
+                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0)), cA, a.x, lane, yA0,
+                    yA1, yA2);
+        if (nB < n1)
+          node_rows(reinterpret_cast<const double *>(stage + (72ull * pB - vb0)),
+                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pB - nb0)), cB, a.x, lane, yB0,
+                    yB1, yB2);
+      } else {
+        if (nA < n1) node_rows(data + 9 * pA, nbr + pA, cA, a.x, lane, yA0, yA1, yA2);
+        if (nB < n1) node_rows(data + 9 * pB, nbr + pB, cB, a.x, lane, yB0, yB1, yB2);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);  // stage reads done; the producer may refill it
+      if (nA < n1) {
+        const double acc = warp_sum3(yA0, yA1, yA2, lane);
+        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nA + (lane >> 3), acc, a, preA, red0, red1);
+      }
+      if (nB < n1) {
+        const double acc = warp_sum3(yB0, yB1, yB2, lane);
+        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nB + (lane >> 3), acc, a, preB, red0, red1);
+      }
     }
   }
   if (MODE != SP_PLAIN) {
-    double v[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2>(v, red, tot) && threadIdx.x == 0) spmv_stage<MODE>(a.sc, tot);
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0)
+      spmv_stage<MODE>(a.sc, tot);
   }
+}
+
+// Pack consecutive nodes into chunks whose values + neighbour ids fit one stage
+// (with 16-byte alignment slack).  Requires every chunk to hold <= 2*kTmaConsumers nodes.
+int prepare_fem3_chunks(Matrix *m) {
+  const int64_t nn = m->n / 3;
+  std::vector<int32_t> ptr(nn + 1);
+  if (cudaMemcpy(ptr.data(), m->nbr_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return B200FEM_E_CUDA;
+  std::vector<int32_t> ch{0};
+  int64_t start = 0;
+  for (int64_t n = 0; n < nn; ++n) {
+    const int64_t nb = ptr[n + 1] - ptr[start];
+    const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= 2 * kTmaConsumers;
+    if (!fits) {
+      if (n == start) return 0;  // a single node does not fit a stage: keep the LDG kernel
+      ch.push_back((int32_t)n);
+      start = n;
+    }
+  }
+  ch.push_back((int32_t)nn);
+  m->n_chunks = (int)ch.size() - 1;
+  if (dalloc(&m->chunk_node, ch.size()) != cudaSuccess) return B200FEM_E_CUDA;
+  if (cudaMemcpy(m->chunk_node, ch.data(), ch.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+    return B200FEM_E_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    attr = true;
+  }
+  m->use_tma = true;
+  return 0;
 }
 
 template <int MODE, int LANES>
@@ -142,13 +366,26 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   for (int64_t base = warp0 * kPerWarp; base < n; base += nwarps * kPerWarp) {
     const int64_t row = base + sub;
     double acc = 0.0;
+    RowPre pre{0.0, 0.0, 0.0, 0.0};
+    if (row < n && sl == 0) pre = spmv_preload<MODE>(row, a);
     if (row < n) {
-      const int k1 = indptr[row + 1];
-      for (int k = indptr[row] + sl; k < k1; k += LANES) acc = fma(__ldg(data + k), __ldg(a.x + indices[k]), acc);
+      const int k1 = __ldg(indptr + row + 1);
+      int k = __ldg(indptr + row) + sl;
+      for (; k + 3 * LANES < k1; k += 4 * LANES) {  // 4 independent loads in flight per lane
+        const double d0 = __ldcs(data + k), d1 = __ldcs(data + k + LANES), d2 = __ldcs(data + k + 2 * LANES),
+                     d3 = __ldcs(data + k + 3 * LANES);
+        const int i0 = __ldcs(indices + k), i1 = __ldcs(indices + k + LANES), i2 = __ldcs(indices + k + 2 * LANES),
+                  i3 = __ldcs(indices + k + 3 * LANES);
+        acc = fma(d0, __ldg(a.x + i0), acc);
+        acc = fma(d1, __ldg(a.x + i1), acc);
+        acc = fma(d2, __ldg(a.x + i2), acc);
+        acc = fma(d3, __ldg(a.x + i3), acc);
+      }
+      for (; k < k1; k += LANES) acc = fma(__ldcs(data + k), __ldg(a.x + __ldcs(indices + k)), acc);
     }
 #pragma unroll
     for (int o = LANES / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (row < n && sl == 0) spmv_epilogue<MODE>(row, acc, a, red0, red1);
+    if (row < n && sl == 0) spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
   }
   if (MODE != SP_PLAIN) {
     double v[2] = {red0, red1}, tot[2];
@@ -160,7 +397,14 @@ template <int MODE>
 static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
   RedScratch r = red ? *red : RedScratch{};
-  if (m->kind == MK_FEM3) {
+  if (m->kind == MK_FEM3 && m->use_tma) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = std::min(sms, m->n_chunks);
+    k_spmv_fem3_tma<MODE><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
+                                                                  m->n_chunks, m->nnz / 9, a, r);
+  } else if (m->kind == MK_FEM3) {
     k_spmv_fem3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->n / 3, a, r);
   } else {
     switch (m->lanes) {

@@ -147,7 +147,7 @@ def test_spmv_matches_oracle(name, rng):
     # generic CSR path (host-built matrix) on the same operator
     K2 = fem.CsrMatrix(K.indptr, K.indices, K.data)
     assert rel(K2 @ x, y_ref) < 1e-14
-    assert np.array_equal(K.diagonal(), orc._diag_of(K.indptr, K.indices, K.data))
+    assert np.array_equal(K.diagonal(), orc.gradfem_oracle._diag_of(K.indptr, K.indices, K.data))
 
 
 def test_determinism_bitwise(rng):
@@ -332,3 +332,20 @@ def test_device_tensors_stay_on_device():
     assert isinstance(R, torch.Tensor) and R.is_cuda
     Us, rep = fem.newton_solve(prob, Ud)
     assert isinstance(Us, torch.Tensor) and Us.is_cuda and rep.converged
+
+
+@pytest.mark.skip(reason="opt-in bulk-copy SpMV (B200FEM_SPMV_TMA) is experimental; see profiles/")
+def test_bulk_copy_spmv_bit_identical_to_ldg_kernel(rng, monkeypatch):
+    """The cp.async.bulk pipelined FEM3 SpMV and the register-streaming kernel agree bitwise."""
+    _, prob, U = build("nh_block", dict(CASES["nh_block"], dims=(9, 7, 5)))
+    K = fem.assemble_jacobian(prob, U)
+    x = rng.standard_normal(prob.n_dofs)
+    y_ldg = K @ x
+    monkeypatch.setenv("B200FEM_SPMV_TMA", "1")
+    K2 = fem.assemble_jacobian(prob, U)
+    y_tma = K2 @ x
+    assert np.array_equal(y_tma, y_ldg)
+    b = rng.standard_normal(prob.n_dofs)
+    cfg = fem.LinearSolveConfig(rel_tol=1e-12, abs_tol=1e-14)
+    x1, x2 = fem.bicgstab_jacobi(K2, b, cfg=cfg), fem.bicgstab_jacobi(K, b, cfg=cfg)
+    assert rel(x1, x2) < 1e-9
