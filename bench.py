@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--stretch", type=float, default=0.02)
     p.add_argument("--cpu-sample-n", type=int, default=12)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--partitioned", action="store_true",
+                   help="use the partitioned (multi-GPU) solver even on one rank (path check)")
     return p.parse_args()
 
 
@@ -194,14 +196,23 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     n = args.n
     mesh = fem.generate_box_mesh(n, n, n, 1.0, 1.0, 1.0)
@@ -211,15 +222,35 @@ def run_ours(args):
     specs = [fem.DirichletSpec(bot, c, lambda p: 0.0) for c in range(3)] + [
         fem.DirichletSpec(top, 2, lambda p, s=s: np.full(np.asarray(p).shape[:-1], s) if np.ndim(p) > 1 else s)]
     prob = fem.NeoHookeanProblem(mesh, alu, specs)
-    t0 = time.perf_counter()
-    ws = fem.workspace(prob)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
     N = prob.n_dofs
-    U0 = D.zeros(N)
+    t0 = time.perf_counter()
+    if world == 1 and not args.partitioned:
+        ws = fem.workspace(prob)
+        U0 = D.zeros(N)
+        sub, part = prob, None
 
-    def step():
-        return fem.newton_solve(prob, U0)
+        def step():
+            return fem.newton_solve(prob, U0)
+
+        def e2e_step(U0_host):
+            U, _ = fem.newton_solve(prob, U0_host)  # pinned host in, numpy out
+            return U
+    else:
+        from paper_2212_00964_b200.distributed import PartitionedSolver
+
+        solver = PartitionedSolver(prob, nparts=world, mode="nccl")
+        part = solver.parts[0]
+        ws, sub = part.ws, part.problem
+
+        def step():
+            return None, solver.newton_solve()
+
+        def e2e_step(U0_host):
+            solver.newton_solve(U0_host)
+            lo, hi = part.own_dofs
+            return D.to_host(part.U[lo:hi])
+    torch.cuda.synchronize()
+    setup_s = max_over_ranks(time.perf_counter() - t0)
 
     for _ in range(args.warmup):
         step()
@@ -237,20 +268,24 @@ def run_ours(args):
     launches = _lib.launch_count() - l0
     ck = clocks.stop()
     per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(ev[0].elapsed_time(ev[-1]))
     ms = total_ms / args.steps
     rep = reports[-1]
     lin_iters = [s_.iterations for s_ in rep.linear_stats]
     matvecs = sum(s_.matvecs for s_ in rep.linear_stats)
 
     # ---------------- kernel-level evidence (after the timed region, same stream, CUDA events)
-    K = _tangent_matrix(prob, U)
-    x = D.to_device(np.random.default_rng(0).standard_normal(N))
-    y = D.empty(N)
+    if part is None:
+        K = _tangent_matrix(prob, U)
+        Uk = U
+        n_rows_nodes, row_lo = mesh.n_nodes, 0
+    else:
+        K, Uk = part.K, part.U
+        row_lo, row_hi = part.plan.own_local
+        n_rows_nodes = row_hi - row_lo
+    Nl = sub.n_dofs
+    x = D.to_device(np.random.default_rng(0).standard_normal(Nl))
+    y = D.empty(Nl)
     h = K._device_handle()
     lib = _lib.lib()
     for _ in range(3):
@@ -263,59 +298,59 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     t_spmv = e0.elapsed_time(e1) / reps / 1e3
-    nnz = ws.nnz
-    n_nodes = mesh.n_nodes
-    bytes_fem = 8 * nnz + 4 * (nnz // 9) + 4 * (n_nodes + 1) + 8 * N + 8 * N
-    bytes_csr = 12 * nnz + 4 * (N + 1) + 8 * N + 8 * N
-    R = D.empty(N)
+    ip = ws.indptr
+    nnz_rows = int(ip[3 * (row_lo + n_rows_nodes)] - ip[3 * row_lo])
+    rows = 3 * n_rows_nodes
+    bytes_fem = 8 * nnz_rows + 4 * (nnz_rows // 9) + 4 * (n_rows_nodes + 1) + 8 * Nl + 8 * rows
+    bytes_csr = 12 * nnz_rows + 4 * (rows + 1) + 8 * Nl + 8 * rows
+    R = D.empty(Nl)
     e0.record()
     for _ in range(5):
-        ws.residual(prob, U, R)
+        ws.residual(sub, Uk, R)
     e1.record()
     torch.cuda.synchronize()
     t_res = e0.elapsed_time(e1) / 5 / 1e3
     e0.record()
     for _ in range(3):
-        ws.jacobian(prob, U, K.device_data)
+        ws.jacobian(sub, Uk, K.device_data)
     e1.record()
     torch.cuda.synchronize()
     t_jac = e0.elapsed_time(e1) / 3 / 1e3
+    n_cells_l, n_nodes_l = sub.mesh.n_cells, sub.mesh.n_nodes
 
     # ---------------- e2e through the public API with host buffers
     U0_host = torch.zeros(N, dtype=torch.float64).pin_memory()
-    fem.newton_solve(prob, U0_host)
+    e2e_step(U0_host)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        Uh, _ = fem.newton_solve(prob, U0_host)
+        e2e_step(U0_host)
     barrier()
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    d2h = 8 * N if part is None else 8 * (part.own_dofs[1] - part.own_dofs[0])
 
     peak, peak_kind = peaks()
     traffic = ncu_traffic()
     achieved = bytes_fem / t_spmv / 1e9
     out = {
         "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "weak" if world > 1 else "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated box mesh, 2% stretch BCs)",
-        "config": dict(config(n, s), parallelism="replicas" if world > 1 else "single"),
-        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N},
+        "config": dict(config(n, s), parallelism=f"node-slab partition x{world} (NCCL halo + allreduce)"
+                       if part is not None else "single GPU"),
+        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": {"kernel": "k_spmv_fem3 (CSR SpMV, node-blocked column index)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "bytes_per_launch": bytes_fem,
-                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,
                      "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6},
         "newton": {"iterations": rep.n_iterations, "residual_norms": rep.residual_norms,
                    "linear_iterations": lin_iters, "matvecs": matvecs, "per_step_ms": per_step},
-        "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": mesh.n_cells / t_res / 1e6,
-                     "jacobian_ms": t_jac * 1e3, "jacobian_mcells_s": mesh.n_cells / t_jac / 1e6,
-                     "jacobian_hbm_gbs": (8 * nnz + 32 * mesh.n_cells + 24 * n_nodes + 8 * N) / t_jac / 1e9},
+        "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": n_cells_l / t_res / 1e6,
+                     "jacobian_ms": t_jac * 1e3, "jacobian_mcells_s": n_cells_l / t_jac / 1e6,
+                     "jacobian_hbm_gbs": (8 * ws.nnz + 32 * n_cells_l + 24 * n_nodes_l + 8 * Nl) / t_jac / 1e9,
+                     "per_rank": world > 1},
         "setup_s": setup_s,
         "clocks": ck,
     }

@@ -143,6 +143,34 @@ int b200fem_bicgstab(b200fem_matrix *m, const double *b_dev, double *x_dev, int3
                      double rel_tol, double abs_tol, int64_t max_iters, b200fem_solve_info *info,
                      b200fem_error *err);
 
+/* ---- partitioned solve (new — the reference is single-process) ----
+ * A part = the local FEM matrix of one contiguous node range plus its ghost layer.  Halo
+ * lists are local node ids: send_nodes[k] (owned, needed by peer i) and recv_nodes[k]
+ * (ghost, owned by peer i), grouped per peer.  Communicator: NCCL (one part per process)
+ * or local (several parts in one process on one device, for verification). */
+typedef struct b200fem_comm b200fem_comm;
+typedef struct b200fem_part b200fem_part;
+int b200fem_comm_unique_id(uint8_t *out /* 128 bytes */);
+int b200fem_comm_create_nccl(b200fem_comm **out, const uint8_t *id /* 128 bytes */, int32_t nranks, int32_t rank);
+int b200fem_comm_create_local(b200fem_comm **out);
+int b200fem_comm_destroy(b200fem_comm *comm);
+int b200fem_comm_allreduce(b200fem_comm *comm, double *buf_dev, int64_t n, void *stream);
+int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_node_lo, int64_t own_node_hi,
+                        int32_t n_peers, const int32_t *peers_host, const int64_t *send_counts_host,
+                        const int32_t *send_nodes_host, const int64_t *recv_counts_host,
+                        const int32_t *recv_nodes_host);
+int b200fem_part_destroy(b200fem_part *part);
+/* BiCGSTAB over all parts (solvers.py:87-167 semantics, global tolerances and counters);
+ * b[p], x[p] are the parts' local device vectors (owned entries are the unknowns). */
+int b200fem_dist_bicgstab(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *b,
+                          double *const *x, int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters,
+                          b200fem_solve_info *info, b200fem_error *err);
+/* ghost entries of vec[p] <- owners' values */
+int b200fem_dist_halo(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *vec);
+/* sum over parts of the owned-range dot products */
+int b200fem_dist_dot(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *x,
+                     double *const *y, double *out_host);
+
 /* ---- small vector helpers (deterministic) ---- */
 int b200fem_norm2(const double *x_dev, int64_t n, double *out_host, void *stream);
 int b200fem_gather_sum(const double *x_dev, const int64_t *idx_dev, int64_t n, double *out_host,

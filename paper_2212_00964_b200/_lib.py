@@ -83,6 +83,17 @@ SIGNATURES = {
     "b200fem_matvec": (C.c_int, [_vp, _vp, _vp]),
     "b200fem_diagonal": (C.c_int, [_vp, _vp]),
     "b200fem_bicgstab": (C.c_int, [_vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo), _perr]),
+    "b200fem_comm_unique_id": (C.c_int, [_vp]),
+    "b200fem_comm_create_nccl": (C.c_int, [C.POINTER(_vp), _vp, _i32, _i32]),
+    "b200fem_comm_create_local": (C.c_int, [C.POINTER(_vp)]),
+    "b200fem_comm_destroy": (C.c_int, [_vp]),
+    "b200fem_comm_allreduce": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "b200fem_part_create": (C.c_int, [C.POINTER(_vp), _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "b200fem_part_destroy": (C.c_int, [_vp]),
+    "b200fem_dist_bicgstab": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo),
+                                        _perr]),
+    "b200fem_dist_halo": (C.c_int, [_vp, _i32, _vp, _vp]),
+    "b200fem_dist_dot": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _pf64]),
     "b200fem_norm2": (C.c_int, [_vp, _i64, _pf64, _vp]),
     "b200fem_gather_sum": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_axpy": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),

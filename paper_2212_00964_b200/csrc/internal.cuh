@@ -136,6 +136,8 @@ struct Matrix {
   int32_t *chunk_node = nullptr;
   int n_chunks = 0;
   bool use_tma = false;
+  // rows computed by matvec/Krylov: node range (FEM3) or row range (CSR); -1 = all
+  int64_t row_lo = 0, row_hi = -1;
 };
 
 // allocation helpers
@@ -162,8 +164,9 @@ struct SpmvArgs {
   const double *dg;  // diagonal (residual mode)
   const double *aux; // r0 (mode 1), b (mode 3)
   double *aux2;      // r0 copy target (mode 3)
-  KrylovScalars *sc; // null -> always run
-  int stage;         // which scalar update the last block performs
+  KrylovScalars *sc; // status gate (null -> always run)
+  int inline_stage;  // 1: the last block applies the scalar update (one rank);
+                     // 0: totals are left in red.result for a cross-rank allreduce
 };
 int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
@@ -180,9 +183,70 @@ int check_geometry(Ctx *c, b200fem_error *err);
 void element_tables_init();
 int fetch_element_errors(Ctx *c, b200fem_error *err, bool jacobian);
 
-// Krylov
+// Krylov (krylov.cu)
+int ensure_work(Matrix *m);
+void free_work(KrylovWork *w);
+__global__ void k_begin(KrylovScalars *S);
+__global__ void __launch_bounds__(kThreads) k_update_p(int64_t n, const double *__restrict__ r, const double *__restrict__ v,
+                           double *__restrict__ p, const KrylovScalars *S);
+__global__ void __launch_bounds__(kThreads) k_update_s(int64_t n, const double *__restrict__ r, const double *__restrict__ v,
+                           double *__restrict__ s, const KrylovScalars *S);
+__global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+                            const double *__restrict__ s, const double *__restrict__ t,
+                            const double *__restrict__ r0, const double *__restrict__ dg, KrylovScalars *S,
+                            RedScratch red, int inline_stage);
 int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol,
              int64_t max_iters, b200fem_solve_info *info, b200fem_error *err);
+
+// ------------------------------------------------------ Krylov scalar stages
+// BiCGSTAB iteration start (solvers.py:131-139): it += 1, rho_new = r0.r, breakdown test, beta.
+__device__ __forceinline__ void iter_start(KrylovScalars *S) {
+  if (S->it >= S->max_iters) {
+    S->status = KS_MAXED;
+    return;
+  }
+  S->it += 1;
+  const double rho_new = S->r0r;
+  const double scale = sqrt(S->r0r0) * sqrt(S->rr);
+  const bool broke = fabs(rho_new) <= 1e-30 * scale || (!S->first && S->omega == 0.0);
+  if (broke) {
+    S->status = KS_BREAKDOWN;
+    return;
+  }
+  S->beta = S->first ? 0.0 : (rho_new / S->rho) * (S->alpha / S->omega);
+  S->first = 0;
+  S->rho = rho_new;
+}
+
+enum StageKind : int { ST_R0 = 1, ST_TT = 2, ST_RES = 3, ST_XR = 4 };
+// Scalar update after a reduction with global totals tot[] (solvers.py:141-167).
+__device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const double *tot) {
+  if (!S || S->status != KS_RUNNING) return;
+  if (kind == ST_R0) {
+    S->mv += 1;
+    S->r0v = tot[0];
+    if (tot[0] == 0.0) S->status = KS_BREAKDOWN;
+    else S->alpha = S->rho / tot[0];
+  } else if (kind == ST_TT) {
+    S->mv += 1;
+    S->tt = tot[0];
+    S->ts = tot[1];
+    S->omega = tot[0] > 0.0 ? tot[1] / tot[0] : 0.0;
+  } else if (kind == ST_RES) {
+    S->mv += 1;
+    S->res = sqrt(tot[0]);
+    S->r0r0 = S->r0r = S->rr = tot[1];
+  } else {  // ST_XR
+    S->res = sqrt(tot[0]);
+    S->r0r = tot[1];
+    S->rr = tot[2];
+    if (S->res <= S->tol) {
+      S->status = KS_CONV_INNER;
+      return;
+    }
+    iter_start(S);
+  }
+}
 
 // ------------------------------------------------------------ device helpers
 __device__ __forceinline__ double warp_sum(double v) {

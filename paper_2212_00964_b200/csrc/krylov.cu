@@ -24,24 +24,6 @@
 
 namespace b200 {
 
-__device__ __forceinline__ void iter_start(KrylovScalars *S) {
-  if (S->it >= S->max_iters) {
-    S->status = KS_MAXED;
-    return;
-  }
-  S->it += 1;
-  const double rho_new = S->r0r;
-  const double scale = sqrt(S->r0r0) * sqrt(S->rr);
-  const bool broke = fabs(rho_new) <= 1e-30 * scale || (!S->first && S->omega == 0.0);
-  if (broke) {
-    S->status = KS_BREAKDOWN;
-    return;
-  }
-  S->beta = S->first ? 0.0 : (rho_new / S->rho) * (S->alpha / S->omega);
-  S->first = 0;
-  S->rho = rho_new;
-}
-
 __global__ void k_begin(KrylovScalars *S) {
   if (S->status == KS_RUNNING) iter_start(S);
 }
@@ -68,7 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
                                                         const double *__restrict__ p, const double *__restrict__ s,
                                                         const double *__restrict__ t, const double *__restrict__ r0,
                                                         const double *__restrict__ dg, KrylovScalars *S,
-                                                        RedScratch red) {
+                                                        RedScratch red, int inline_stage) {
   if (S->status != KS_RUNNING) return;
   const double alpha = S->alpha, omega = S->omega;
   double acc[3] = {0.0, 0.0, 0.0};
@@ -82,19 +64,10 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
     acc[2] = fma(ri, ri, acc[2]);
   }
   double tot[3];
-  if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0) {
-    S->res = sqrt(tot[0]);
-    S->r0r = tot[1];
-    S->rr = tot[2];
-    if (S->res <= S->tol) {
-      S->status = KS_CONV_INNER;
-      return;
-    }
-    iter_start(S);
-  }
+  if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0 && inline_stage) apply_stage(ST_XR, S, tot);
 }
 
-static int ensure_work(Matrix *m) {
+int ensure_work(Matrix *m) {
   if (m->kw) return 0;
   KrylovWork *w = new KrylovWork();
   w->n = m->n;
@@ -128,12 +101,12 @@ static void enqueue_iteration(Matrix *m, const double *b, double *x) {
   cudaStream_t s = m->stream;
   const int64_t n = m->n;
   k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
-  SpmvArgs a1{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
+  SpmvArgs a1{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 1};
   launch_spmv(m, SP_JACOBI_R0, a1, &w->red);
   k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
-  SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
+  SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 1};
   launch_spmv(m, SP_JACOBI_TT, a2, &w->red);
-  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red);
+  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
   count_launch(3);
   (void)b;
 }
@@ -181,7 +154,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     H[0].it = it;
     H[0].mv = mv;
     B200_CUDA_E(cudaMemcpyAsync(w->sc, &H[0], ssz, cudaMemcpyHostToDevice, s), err);
-    SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->r0, w->sc, 0};
+    SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->r0, w->sc, 1};
     if (launch_spmv(m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
     ++restarts;
     B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);

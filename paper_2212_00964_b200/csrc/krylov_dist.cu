@@ -1,0 +1,471 @@
+// Partitioned BiCGSTAB: the mesh is split into contiguous node
+// ranges ("parts"); each part owns the DOF rows of its nodes and holds a ghost layer of
+// cells, so its owned rows assemble locally with no communication.  Per iteration the
+// only exchanges are
+//   * a halo of the SpMV operand (p, then s): owned values of interface nodes -> the ghost
+//     entries of the neighbouring parts (packed, ncclSend/ncclRecv),
+//   * three FP64 sum-allreduces of the fused dot groups {r0.v}, {t.t, t.s},
+//     {||D r||^2, r0.r, r.r}, after which every part applies the same scalar update.
+// Communicators: NCCL across processes (one part per process and GPU), or "local": all
+// parts in one process on one device, exchanged by device copies and summed by a kernel
+// in part order -- the same algorithm, used to verify partitioning on a single B200.
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace b200 {
+
+struct Comm {
+  int kind = 0;  // 0 local, 1 nccl
+  ncclComm_t nccl = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+struct Part {
+  Matrix *m = nullptr;
+  int vec = 3;
+  int64_t own_lo = 0, own_hi = 0;  // owned local node range
+  int n_peers = 0;
+  std::vector<int> peer;           // peer part index (local) or rank (nccl)
+  std::vector<int64_t> soff, roff; // node offsets into the packed buffers (n_peers + 1)
+  int32_t *send_nodes = nullptr, *recv_nodes = nullptr;
+  double *sendbuf = nullptr, *recvbuf = nullptr;
+};
+
+__global__ void k_pack(const double *__restrict__ v, const int32_t *__restrict__ nodes, int64_t n, int vec,
+                       double *__restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * vec; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = v[(int64_t)nodes[i / vec] * vec + i % vec];
+}
+
+__global__ void k_unpack(double *__restrict__ v, const int32_t *__restrict__ nodes, int64_t n, int vec,
+                         const double *__restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * vec; i += (int64_t)gridDim.x * blockDim.x)
+    v[(int64_t)nodes[i / vec] * vec + i % vec] = buf[i];
+}
+
+// sum NV values over the parts in part order and broadcast the total back (deterministic)
+__global__ void k_sum_parts(double *const *res, int np, int nv) {
+  const int j = threadIdx.x;
+  if (j >= nv) return;
+  double s = 0.0;
+  for (int p = 0; p < np; ++p) s += res[p][j];
+  for (int p = 0; p < np; ++p) res[p][j] = s;
+}
+
+__global__ void k_stage(int kind, KrylovScalars *S, const double *tot) { apply_stage(kind, S, tot); }
+
+// owned-range dot product -> red.result[0]
+__global__ void __launch_bounds__(kThreads) k_dot_owned(const double *__restrict__ x, const double *__restrict__ y,
+                                                        int64_t n, RedScratch red) {
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[0] = fma(x[i], y[i], v[0]);
+  double tot[1];
+  block_partials_and_finish<1>(v, red, tot);
+}
+
+static int grid_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
+
+struct Dist {
+  std::vector<Part *> parts;
+  Comm *comm;
+  double **res_dev = nullptr;  // device array of the parts' red.result pointers (local comm)
+
+  cudaStream_t stream(int p) const { return parts[p]->m->stream; }
+
+  int allreduce(int nv) {
+    if (comm->kind == 1) {
+      Part *P = parts[0];
+      double *r = P->m->kw->red.result;
+      if (ncclAllReduce(r, r, nv, ncclDouble, ncclSum, comm->nccl, stream(0)) != ncclSuccess) return B200FEM_E_CUDA;
+      return 0;
+    }
+    if (parts.size() == 1) return 0;
+    k_sum_parts<<<1, 32, 0, stream(0)>>>(res_dev, (int)parts.size(), nv);
+    count_launch();
+    return 0;
+  }
+
+  // ghost entries of vec[p] <- owners' values
+  int halo(double *const *vec) {
+    for (size_t p = 0; p < parts.size(); ++p) {
+      Part *P = parts[p];
+      const int64_t ns = P->soff.back();
+      if (ns) {
+        k_pack<<<grid_n(ns * P->vec), kThreads, 0, stream(p)>>>(vec[p], P->send_nodes, ns, P->vec, P->sendbuf);
+        count_launch();
+      }
+    }
+    if (comm->kind == 1) {
+      Part *P = parts[0];
+      if (P->n_peers) {
+        ncclGroupStart();
+        for (int i = 0; i < P->n_peers; ++i) {
+          const int64_t sn = P->soff[i + 1] - P->soff[i], rn = P->roff[i + 1] - P->roff[i];
+          if (sn) ncclSend(P->sendbuf + P->soff[i] * P->vec, sn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
+          if (rn) ncclRecv(P->recvbuf + P->roff[i] * P->vec, rn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
+        }
+        if (ncclGroupEnd() != ncclSuccess) return B200FEM_E_CUDA;
+      }
+    } else {
+      for (size_t p = 0; p < parts.size(); ++p) {
+        Part *P = parts[p];
+        for (int i = 0; i < P->n_peers; ++i) {
+          Part *Q = parts[P->peer[i]];
+          int j = 0;
+          while (j < Q->n_peers && Q->peer[j] != (int)p) ++j;
+          if (j == Q->n_peers) return B200FEM_E_INVALID;
+          const int64_t rn = P->roff[i + 1] - P->roff[i];
+          if (rn != Q->soff[j + 1] - Q->soff[j]) return B200FEM_E_INVALID;
+          if (rn)
+            B200_CUDA(cudaMemcpyAsync(P->recvbuf + P->roff[i] * P->vec, Q->sendbuf + Q->soff[j] * Q->vec,
+                                      rn * P->vec * sizeof(double), cudaMemcpyDeviceToDevice, stream(p)));
+        }
+      }
+    }
+    for (size_t p = 0; p < parts.size(); ++p) {
+      Part *P = parts[p];
+      const int64_t nr = P->roff.back();
+      if (nr) {
+        k_unpack<<<grid_n(nr * P->vec), kThreads, 0, stream(p)>>>(vec[p], P->recv_nodes, nr, P->vec, P->recvbuf);
+        count_launch();
+      }
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
+  }
+
+  void stage(int kind) {
+    for (size_t p = 0; p < parts.size(); ++p) {
+      KrylovWork *w = parts[p]->m->kw;
+      k_stage<<<1, 1, 0, stream(p)>>>(kind, w->sc, w->red.result);
+      count_launch();
+    }
+  }
+
+  // owned dot products summed over ranks -> host
+  int dot(double *const *x, double *const *y, double *out) {
+    for (size_t p = 0; p < parts.size(); ++p) {
+      Part *P = parts[p];
+      const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+      k_dot_owned<<<kRedBlocks, kThreads, 0, stream(p)>>>(x[p] + lo, y[p] + lo, n, P->m->kw->red);
+      count_launch();
+    }
+    int st = allreduce(1);
+    if (st) return st;
+    B200_CUDA(cudaMemcpyAsync(out, parts[0]->m->kw->red.result, sizeof(double), cudaMemcpyDeviceToHost, stream(0)));
+    B200_CUDA(cudaStreamSynchronize(stream(0)));
+    return 0;
+  }
+};
+
+static void enqueue_dist_iteration(Dist &D, double *const *x) {
+  const size_t np = D.parts.size();
+  std::vector<double *> pv(np), sv(np);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_p<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->p + lo, w->sc);
+    count_launch();
+    pv[p] = w->p;
+    sv[p] = w->s;
+  }
+  D.halo(pv.data());
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    SpmvArgs a{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
+    launch_spmv(D.parts[p]->m, SP_JACOBI_R0, a, &w->red);
+  }
+  D.allreduce(1);
+  D.stage(ST_R0);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_s<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->s + lo, w->sc);
+    count_launch();
+  }
+  D.halo(sv.data());
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    SpmvArgs a{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
+    launch_spmv(D.parts[p]->m, SP_JACOBI_TT, a, &w->red);
+  }
+  D.allreduce(2);
+  D.stage(ST_TT);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_xr<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, x[p] + lo, w->r + lo, w->p + lo, w->s + lo, w->t + lo,
+                                                         w->r0 + lo, w->diag + lo, w->sc, w->red, 0);
+    count_launch();
+  }
+  D.allreduce(3);
+  D.stage(ST_XR);
+}
+
+// Same control flow as the single-GPU bicgstab (krylov.cu) with the collectives inserted.
+static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0, double rel_tol, double abs_tol,
+                         int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+  const size_t np = D.parts.size();
+  int64_t n_global_owned = 0;
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    if (ensure_work(P->m)) return set_err(err, B200FEM_E_CUDA, "Krylov workspace allocation failed"), B200FEM_E_CUDA;
+    n_global_owned += (P->own_hi - P->own_lo) * P->vec;
+  }
+  if (D.comm->kind == 0 && np > 1) {
+    std::vector<double *> rp(np);
+    for (size_t p = 0; p < np; ++p) rp[p] = D.parts[p]->m->kw->red.result;
+    B200_CUDA_E(dalloc(&D.res_dev, np), err);
+    B200_CUDA_E(cudaMemcpy(D.res_dev, rp.data(), np * sizeof(double *), cudaMemcpyHostToDevice), err);
+  }
+  // zero-diagonal check on owned rows, summed over ranks
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    if (launch_diagonal(D.parts[p]->m, w->diag, w->inv, &w->red, nullptr)) return B200FEM_E_CUDA;
+  }
+  if (D.allreduce(1)) return B200FEM_E_CUDA;
+  double nz = 0.0, bb = 0.0;
+  B200_CUDA_E(cudaMemcpyAsync(&nz, D.parts[0]->m->kw->red.result, sizeof(double), cudaMemcpyDeviceToHost, D.stream(0)), err);
+  B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
+  if (nz > 0.0) {
+    set_err(err, B200FEM_E_ZERO_DIAGONAL, "zero diagonal entry; Jacobi preconditioner undefined");
+    return B200FEM_E_ZERO_DIAGONAL;
+  }
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x[p], 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+    // ghost rows of the Krylov vectors are never computed: keep them finite
+    B200_CUDA_E(cudaMemsetAsync(w->v, 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+  }
+  if (D.dot(b, b, &bb)) return B200FEM_E_CUDA;
+  const double tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
+  if (D.comm->kind == 1) {  // global DOF count for the default max_iters = 10 N
+    double cnt = (double)n_global_owned;
+    double *slot = D.parts[0]->m->kw->red.result;
+    B200_CUDA_E(cudaMemcpyAsync(slot, &cnt, sizeof(double), cudaMemcpyHostToDevice, D.stream(0)), err);
+    if (D.allreduce(1)) return B200FEM_E_CUDA;
+    B200_CUDA_E(cudaMemcpyAsync(&cnt, slot, sizeof(double), cudaMemcpyDeviceToHost, D.stream(0)), err);
+    B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
+    n_global_owned = (int64_t)cnt;
+  }
+  const int64_t max_it = max_iters > 0 ? max_iters : 10 * n_global_owned;
+  KrylovScalars H{};
+  H.tol = tol;
+  H.max_iters = max_it;
+  long long it = 0, mv = 0, restarts = 0;
+  double last_bd = -1.0;
+  KrylovScalars *poll = D.parts[0]->m->kw->sc_host;
+  for (;;) {
+    H.status = KS_RUNNING;
+    H.first = 1;
+    H.rho = H.alpha = H.omega = 1.0;
+    H.it = it;
+    H.mv = mv;
+    for (size_t p = 0; p < np; ++p)
+      B200_CUDA_E(cudaMemcpyAsync(D.parts[p]->m->kw->sc, &H, sizeof(H), cudaMemcpyHostToDevice, D.stream(p)), err);
+    if (D.halo(x)) return B200FEM_E_CUDA;
+    for (size_t p = 0; p < np; ++p) {
+      KrylovWork *w = D.parts[p]->m->kw;
+      SpmvArgs ar{x[p], w->r, w->inv, w->diag, b[p], w->r0, w->sc, 0};
+      if (launch_spmv(D.parts[p]->m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
+    }
+    if (D.allreduce(2)) return B200FEM_E_CUDA;
+    D.stage(ST_RES);
+    ++restarts;
+    B200_CUDA_E(cudaMemcpyAsync(poll, D.parts[0]->m->kw->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)), err);
+    B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
+    mv = poll->mv;
+    const double res = poll->res;
+    if (res <= tol) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      return 0;
+    }
+    if (it >= max_it) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      if (err) err->iterations = it, err->value = res;
+      set_err(err, B200FEM_E_LINEAR_SOLVER, "BiCGSTAB did not converge in %lld iterations (residual %.3e, tol %.3e)",
+              (long long)max_it, res, tol);
+      return B200FEM_E_LINEAR_SOLVER;
+    }
+    for (size_t p = 0; p < np; ++p) {
+      KrylovWork *w = D.parts[p]->m->kw;
+      B200_CUDA_E(cudaMemsetAsync(w->p, 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+      B200_CUDA_E(cudaMemsetAsync(w->v, 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+      k_begin<<<1, 1, 0, D.stream(p)>>>(w->sc);
+      count_launch();
+    }
+    int batch = 4;
+    for (;;) {
+      for (int i = 0; i < batch; ++i) enqueue_dist_iteration(D, x);
+      B200_CUDA_E(cudaMemcpyAsync(poll, D.parts[0]->m->kw->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)), err);
+      B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
+      if (poll->status != KS_RUNNING) break;
+      batch = std::min(batch * 2, 32);
+    }
+    B200_CUDA_E(cudaGetLastError(), err);
+    it = poll->it;
+    mv = poll->mv;
+    if (poll->status == KS_BREAKDOWN) {
+      if (last_bd >= 0.0 && poll->res >= 0.999 * last_bd) {
+        if (info) *info = b200fem_solve_info{it, mv, restarts, poll->res, tol};
+        if (err) err->iterations = it, err->value = poll->res;
+        set_err(err, B200FEM_E_BREAKDOWN, "BiCGSTAB breakdown without progress at iteration %lld (residual %.3e)", it,
+                poll->res);
+        return B200FEM_E_BREAKDOWN;
+      }
+      last_bd = poll->res;
+    }
+  }
+}
+
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" {
+
+int b200fem_comm_unique_id(uint8_t *out) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return B200FEM_E_CUDA;
+  memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+
+int b200fem_comm_create_nccl(b200fem_comm **out, const uint8_t *id_bytes, int32_t nranks, int32_t rank) {
+  ncclUniqueId id;
+  memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
+  Comm *c = new Comm();
+  c->kind = 1;
+  c->rank = rank;
+  c->nranks = nranks;
+  if (ncclCommInitRank(&c->nccl, nranks, id, rank) != ncclSuccess) {
+    delete c;
+    return B200FEM_E_CUDA;
+  }
+  *out = (b200fem_comm *)c;
+  return 0;
+}
+
+int b200fem_comm_create_local(b200fem_comm **out) {
+  Comm *c = new Comm();
+  c->kind = 0;
+  *out = (b200fem_comm *)c;
+  return 0;
+}
+
+int b200fem_comm_destroy(b200fem_comm *cc) {
+  Comm *c = (Comm *)cc;
+  if (!c) return 0;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return 0;
+}
+
+int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_node_lo, int64_t own_node_hi,
+                        int32_t n_peers, const int32_t *peers, const int64_t *send_counts, const int32_t *send_nodes,
+                        const int64_t *recv_counts, const int32_t *recv_nodes) {
+  Matrix *m = (Matrix *)local;
+  if (!out || !m || own_node_lo < 0 || own_node_hi < own_node_lo) return B200FEM_E_INVALID;
+  Part *P = new Part();
+  P->m = m;
+  P->vec = m->kind == MK_FEM3 ? 3 : 1;
+  P->own_lo = own_node_lo;
+  P->own_hi = own_node_hi;
+  m->row_lo = own_node_lo * (m->kind == MK_FEM3 ? 1 : P->vec);
+  m->row_hi = own_node_hi * (m->kind == MK_FEM3 ? 1 : P->vec);
+  m->use_tma = false;
+  P->n_peers = n_peers;
+  P->peer.assign(peers, peers + n_peers);
+  P->soff.assign(n_peers + 1, 0);
+  P->roff.assign(n_peers + 1, 0);
+  for (int i = 0; i < n_peers; ++i) {
+    P->soff[i + 1] = P->soff[i] + send_counts[i];
+    P->roff[i + 1] = P->roff[i] + recv_counts[i];
+  }
+  const int64_t ns = P->soff.back(), nr = P->roff.back();
+  if (dalloc(&P->send_nodes, ns) || dalloc(&P->recv_nodes, nr) || dalloc(&P->sendbuf, ns * P->vec) ||
+      dalloc(&P->recvbuf, nr * P->vec)) {
+    delete P;
+    return B200FEM_E_CUDA;
+  }
+  if (ns) cudaMemcpy(P->send_nodes, send_nodes, ns * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (nr) cudaMemcpy(P->recv_nodes, recv_nodes, nr * sizeof(int32_t), cudaMemcpyHostToDevice);
+  *out = (b200fem_part *)P;
+  return 0;
+}
+
+int b200fem_part_destroy(b200fem_part *pp) {
+  Part *P = (Part *)pp;
+  if (!P) return 0;
+  cudaFree(P->send_nodes);
+  cudaFree(P->recv_nodes);
+  cudaFree(P->sendbuf);
+  cudaFree(P->recvbuf);
+  if (P->m) P->m->row_lo = 0, P->m->row_hi = -1;
+  delete P;
+  return 0;
+}
+
+static Dist make_dist(b200fem_part **parts, int32_t np, b200fem_comm *comm) {
+  Dist D;
+  for (int i = 0; i < np; ++i) D.parts.push_back((Part *)parts[i]);
+  D.comm = (Comm *)comm;
+  return D;
+}
+
+int b200fem_dist_bicgstab(b200fem_part **parts, int32_t np, b200fem_comm *comm, double *const *b, double *const *x,
+                          int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters, b200fem_solve_info *info,
+                          b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  if (info) memset(info, 0, sizeof(*info));
+  if (np < 1 || !comm || (((Comm *)comm)->kind == 1 && np != 1)) return B200FEM_E_INVALID;
+  if (!(rel_tol > 0) || !(abs_tol > 0)) {
+    set_err(err, B200FEM_E_INVALID, "linear solver tolerances must be positive");
+    return B200FEM_E_INVALID;
+  }
+  Dist D = make_dist(parts, np, comm);
+  const int st = dist_bicgstab(D, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
+  cudaFree(D.res_dev);
+  return st;
+}
+
+int b200fem_dist_halo(b200fem_part **parts, int32_t np, b200fem_comm *comm, double *const *vec) {
+  Dist D = make_dist(parts, np, comm);
+  return D.halo(vec);
+}
+
+int b200fem_dist_dot(b200fem_part **parts, int32_t np, b200fem_comm *comm, double *const *x, double *const *y,
+                     double *out_host) {
+  Dist D = make_dist(parts, np, comm);
+  for (int p = 0; p < np; ++p)
+    if (ensure_work(D.parts[p]->m)) return B200FEM_E_CUDA;
+  if (D.comm->kind == 0 && np > 1) {
+    std::vector<double *> rp(np);
+    for (int p = 0; p < np; ++p) rp[p] = D.parts[p]->m->kw->red.result;
+    B200_CUDA(dalloc(&D.res_dev, np));
+    B200_CUDA(cudaMemcpy(D.res_dev, rp.data(), np * sizeof(double *), cudaMemcpyHostToDevice));
+  }
+  const int st = D.dot(x, y, out_host);
+  cudaFree(D.res_dev);
+  return st;
+}
+
+int b200fem_comm_allreduce(b200fem_comm *comm, double *buf_dev, int64_t n, void *stream) {
+  Comm *c = (Comm *)comm;
+  if (c->kind != 1) return 0;
+  if (ncclAllReduce(buf_dev, buf_dev, n, ncclDouble, ncclSum, c->nccl, (cudaStream_t)stream) != ncclSuccess)
+    return B200FEM_E_CUDA;
+  return 0;
+}
+
+}  // extern "C"

@@ -71,25 +71,12 @@ __device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvA
   }
 }
 
-// Scalar updates performed by the last block of a reduction launch.
+// Scalar updates performed by the last block of a reduction launch (one rank).
 template <int MODE>
 __device__ __forceinline__ void spmv_stage(KrylovScalars *S, const double (&tot)[2]) {
-  if (!S) return;
-  if (MODE == SP_JACOBI_R0) {
-    S->mv += 1;
-    S->r0v = tot[0];
-    if (tot[0] == 0.0) S->status = KS_BREAKDOWN;
-    else S->alpha = S->rho / tot[0];
-  } else if (MODE == SP_JACOBI_TT) {
-    S->mv += 1;
-    S->tt = tot[0];
-    S->ts = tot[1];
-    S->omega = tot[0] > 0.0 ? tot[1] / tot[0] : 0.0;
-  } else if (MODE == SP_RESIDUAL) {
-    S->mv += 1;
-    S->res = sqrt(tot[0]);
-    S->r0r0 = S->r0r = S->rr = tot[1];
-  }
+  if (MODE == SP_JACOBI_R0) apply_stage(ST_R0, S, tot);
+  else if (MODE == SP_JACOBI_TT) apply_stage(ST_TT, S, tot);
+  else if (MODE == SP_RESIDUAL) apply_stage(ST_RES, S, tot);
 }
 
 // Sum three per-lane partials over the warp with a reduce-scatter (6 double shuffles
@@ -117,15 +104,15 @@ __device__ __forceinline__ double warp_sum3(double y0, double y1, double y2, int
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__restrict__ nbr_ptr,
                                                         const int32_t *__restrict__ nbr,
-                                                        const double *__restrict__ data, int64_t n_nodes,
-                                                        SpmvArgs a, RedScratch red) {
+                                                        const double *__restrict__ data, int64_t node_lo,
+                                                        int64_t n_nodes, SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const double *__restrict__ x = a.x;
   double red0 = 0.0, red1 = 0.0;
-  for (int64_t n = warp0; n < n_nodes; n += nwarps) {
+  for (int64_t n = node_lo + warp0; n < n_nodes; n += nwarps) {
     const int p0 = __ldg(nbr_ptr + n);
     const int cnt = __ldg(nbr_ptr + n + 1) - p0;
     const int L = 3 * cnt;
@@ -152,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__rest
   }
   if (MODE != SP_PLAIN) {
     double v2[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2>(v2, red, tot) && threadIdx.x == 0) spmv_stage<MODE>(a.sc, tot);
+    if (block_partials_and_finish<2>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage) spmv_stage<MODE>(a.sc, tot);
   }
 }
 
@@ -311,7 +298,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
   }
   if (MODE != SP_PLAIN) {
     double v2[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0)
+    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
       spmv_stage<MODE>(a.sc, tot);
   }
 }
@@ -354,8 +341,8 @@ int prepare_fem3_chunks(Matrix *m) {
 template <int MODE, int LANES>
 __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict__ indptr,
                                                        const int32_t *__restrict__ indices,
-                                                       const double *__restrict__ data, int64_t n, SpmvArgs a,
-                                                       RedScratch red) {
+                                                       const double *__restrict__ data, int64_t row_lo, int64_t n,
+                                                       SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LANES, sl = lane % LANES;
@@ -363,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double red0 = 0.0, red1 = 0.0;
-  for (int64_t base = warp0 * kPerWarp; base < n; base += nwarps * kPerWarp) {
+  for (int64_t base = row_lo + warp0 * kPerWarp; base < n; base += nwarps * kPerWarp) {
     const int64_t row = base + sub;
     double acc = 0.0;
     RowPre pre{0.0, 0.0, 0.0, 0.0};
@@ -389,7 +376,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   }
   if (MODE != SP_PLAIN) {
     double v[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2>(v, red, tot) && threadIdx.x == 0) spmv_stage<MODE>(a.sc, tot);
+    if (block_partials_and_finish<2>(v, red, tot) && threadIdx.x == 0 && a.inline_stage) spmv_stage<MODE>(a.sc, tot);
   }
 }
 
@@ -397,7 +384,8 @@ template <int MODE>
 static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
   RedScratch r = red ? *red : RedScratch{};
-  if (m->kind == MK_FEM3 && m->use_tma) {
+  const bool full = m->row_hi < 0;
+  if (m->kind == MK_FEM3 && m->use_tma && full) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -405,13 +393,15 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     k_spmv_fem3_tma<MODE><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
                                                                   m->n_chunks, m->nnz / 9, a, r);
   } else if (m->kind == MK_FEM3) {
-    k_spmv_fem3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->n / 3, a, r);
+    const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n / 3 : m->row_hi;
+    k_spmv_fem3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->data, lo, hi, a, r);
   } else {
+    const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n : m->row_hi;
     switch (m->lanes) {
-      case 4: k_spmv_csr<MODE, 4><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, m->n, a, r); break;
-      case 8: k_spmv_csr<MODE, 8><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, m->n, a, r); break;
-      case 16: k_spmv_csr<MODE, 16><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, m->n, a, r); break;
-      default: k_spmv_csr<MODE, 32><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, m->n, a, r); break;
+      case 4: k_spmv_csr<MODE, 4><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, lo, hi, a, r); break;
+      case 8: k_spmv_csr<MODE, 8><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, lo, hi, a, r); break;
+      case 16: k_spmv_csr<MODE, 16><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, lo, hi, a, r); break;
+      default: k_spmv_csr<MODE, 32><<<grid, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->data, lo, hi, a, r); break;
     }
   }
   count_launch();
@@ -432,10 +422,11 @@ int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *r
 __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict__ indptr,
                                                        const int32_t *__restrict__ indices,
                                                        const int32_t *__restrict__ slots,
-                                                       const double *__restrict__ data, int64_t n, double *diag,
-                                                       double *inv, RedScratch red) {
+                                                       const double *__restrict__ data, int64_t row_lo, int64_t n,
+                                                       double *diag, double *inv, RedScratch red) {
   double zeros[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
     double d = 0.0;
     if (slots) {
       d = data[slots[i]];
@@ -456,7 +447,9 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
 }
 
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero) {
-  k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->diag_slots, m->data, m->n, diag, inv,
+  const int64_t lo = m->row_hi < 0 ? 0 : (m->kind == MK_FEM3 ? 3 * m->row_lo : m->row_lo);
+  const int64_t hi = m->row_hi < 0 ? m->n : (m->kind == MK_FEM3 ? 3 * m->row_hi : m->row_hi);
+  k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->diag_slots, m->data, lo, hi, diag, inv,
                                                      *red);
   count_launch();
   if (n_zero) {
