@@ -143,6 +143,13 @@ int b200fem_bicgstab(b200fem_matrix *m, const double *b_dev, double *x_dev, int3
                      double rel_tol, double abs_tol, int64_t max_iters, b200fem_solve_info *info,
                      b200fem_error *err);
 
+/* Jacobi-preconditioned CG for symmetric operators (north_star "CG/BiCGSTAB"; BASELINE
+ * config 2).  FEM matrices: starts from x_d = b_d on Dirichlet rows so the row-replaced K
+ * acts as its SPD free block.  Same termination rule as bicgstab (true residual); restarts
+ * from the explicit residual; BreakdownError if p.Ap <= 0. */
+int b200fem_pcg(b200fem_matrix *m, const double *b_dev, double *x_dev, int32_t has_x0, double rel_tol,
+                double abs_tol, int64_t max_iters, b200fem_solve_info *info, b200fem_error *err);
+
 /* ---- partitioned solve (new — the reference is single-process) ----
  * A part = the local FEM matrix of one contiguous node range plus its ghost layer.  Halo
  * lists are local node ids: send_nodes[k] (owned, needed by peer i) and recv_nodes[k]

@@ -68,6 +68,39 @@ __global__ void k_fill_n2c(const int32_t *__restrict__ cells, int64_t n8, const 
   }
 }
 
+// each node's incident cells in ascending cell order (the reference's accumulation order)
+__global__ void k_sort_n2c(const int32_t *__restrict__ ptr, int64_t n_nodes, const int32_t *__restrict__ cells,
+                           int32_t *n2c, uint8_t *n2c_a, int *max_deg) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    const int lo = ptr[n], hi = ptr[n + 1];
+    for (int i = lo + 1; i < hi; ++i) {
+      const int v = n2c[i];
+      int j = i - 1;
+      while (j >= lo && n2c[j] > v) {
+        n2c[j + 1] = n2c[j];
+        --j;
+      }
+      n2c[j + 1] = v;
+    }
+    // a cell listing the same node twice appears twice: give each copy its own local index
+    for (int i = lo; i < hi; ++i) {
+      const int64_t e = n2c[i];
+      int k = 0, seen = 0;
+      for (int t = lo; t < i; ++t) seen += (n2c[t] == e);
+      for (int q = 0; q < 8; ++q)
+        if (cells[e * 8 + q] == n) {
+          if (seen == 0) {
+            k = q;
+            break;
+          }
+          --seen;
+        }
+      n2c_a[i] = (uint8_t)k;
+    }
+    atomicMax(max_deg, hi - lo);
+  }
+}
+
 constexpr int kMaxCand = 512;  // <= 64 cells per node
 constexpr int kNbrWarps = 4;
 
@@ -211,7 +244,8 @@ static int color_cells_host(const int64_t *cells, int64_t n_cells, int64_t n_nod
 static void free_ctx(Ctx *c) {
   if (!c) return;
   void *ptrs[] = {c->coords, c->cells, c->nbr_ptr, c->nbr, c->indptr, c->cpos, c->diag, c->color_cells,
-                  c->dir_dofs, c->dir_vals, c->f_neumann, c->f_body, c->theta, c->eps_prev, c->sig_prev, c->derr};
+                  c->dir_dofs, c->dir_vals, c->f_neumann, c->f_body, c->theta, c->eps_prev, c->sig_prev, c->derr,
+                  c->n2c_ptr, c->n2c, c->n2c_a, c->dir_flag, c->scratch};
   for (void *p : ptrs) cudaFree(p);
   if (c->indices && c->indices != c->nbr) cudaFree(c->indices);
   red_free(&c->red);
@@ -274,7 +308,7 @@ static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
   auto cleanup = [&]() {
-    cudaFree(deg); cudaFree(n2c_ptr); cudaFree(n2c); cudaFree(cnt); cudaFree(overflow); cudaFree(tmp);
+    cudaFree(deg); cudaFree(cnt); cudaFree(overflow); cudaFree(tmp);
   };
   B200_CUDA_E(dalloc(&deg, nn + 1), err);
   B200_CUDA_E(dalloc(&n2c_ptr, nn + 1), err);
@@ -295,6 +329,15 @@ static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem
   B200_CUDA_E(cudaMemsetAsync(deg, 0, (nn + 1) * sizeof(int32_t), s), err);
   k_fill_n2c<<<grid_for(ne * 8), kThreads, 0, s>>>(c->cells, ne * 8, n2c_ptr, deg, n2c);
   count_launch();
+  c->n2c_ptr = n2c_ptr;
+  c->n2c = n2c;
+  B200_CUDA_E(cudaMemsetAsync(overflow, 0, sizeof(int), s), err);
+  B200_CUDA_E(dalloc(&c->n2c_a, ne * 8), err);
+  k_sort_n2c<<<grid_for(nn), kThreads, 0, s>>>(n2c_ptr, nn, c->cells, n2c, c->n2c_a, overflow);
+  count_launch();
+  B200_CUDA_E(cudaMemcpyAsync(&c->max_deg, overflow, sizeof(int), cudaMemcpyDeviceToHost, s), err);
+  B200_CUDA_E(cudaStreamSynchronize(s), err);
+  B200_CUDA_E(cudaMemsetAsync(overflow, 0, sizeof(int), s), err);
 
   // ---- node adjacency lists (the CSR pattern at node granularity)
   int nb_grid = (int)std::min<int64_t>((nn + kNbrWarps - 1) / kNbrWarps, 148 * 64);
@@ -535,6 +578,8 @@ int b200fem_set_dirichlet(b200fem_ctx *ctx, const int64_t *dofs, const double *v
   c->n_dir = n;
   if (n <= 0) {
     c->n_dir = 0;
+    cudaFree(c->dir_flag);
+    c->dir_flag = nullptr;
     return 0;
   }
   std::vector<int32_t> d32(n);
@@ -544,6 +589,12 @@ int b200fem_set_dirichlet(b200fem_ctx *ctx, const int64_t *dofs, const double *v
   }
   B200_CUDA(dalloc(&c->dir_dofs, n));
   B200_CUDA(dalloc(&c->dir_vals, n));
+  {
+    std::vector<uint8_t> flag(c->n_dofs, 0);
+    for (int64_t i = 0; i < n; ++i) flag[d32[i]] = 1;
+    if (!c->dir_flag) B200_CUDA(dalloc(&c->dir_flag, c->n_dofs));
+    B200_CUDA(cudaMemcpy(c->dir_flag, flag.data(), c->n_dofs, cudaMemcpyHostToDevice));
+  }
   B200_CUDA(cudaMemcpyAsync(c->dir_dofs, d32.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
   B200_CUDA(cudaMemcpyAsync(c->dir_vals, vals, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   B200_CUDA(cudaStreamSynchronize(c->stream));

@@ -20,6 +20,8 @@ namespace b200 {
 
 __constant__ double c_dN[8][8][3];  // [q][k][d] dphi_k/dxi_d at Gauss point q (x fastest)
 __constant__ double c_N[8][8];      // [q][k]    phi_k at Gauss point q
+__constant__ int c_pair_a[36], c_pair_b[36];  // symmetric block pairs a <= b
+__constant__ int c_pair_idx[8][8];            // (a <= b) -> pair index
 
 void element_tables_init() {
   static bool done = false;
@@ -42,6 +44,19 @@ void element_tables_init() {
   }
   cudaMemcpyToSymbol(c_dN, dN, sizeof(dN));
   cudaMemcpyToSymbol(c_N, N, sizeof(N));
+  int pa[36], pb[36], pidx[8][8];
+  int p = 0;
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) pidx[a][b] = -1;
+  for (int a = 0; a < 8; ++a)
+    for (int b = a; b < 8; ++b) {
+      pa[p] = a;
+      pb[p] = b;
+      pidx[a][b] = p++;
+    }
+  cudaMemcpyToSymbol(c_pair_a, pa, sizeof(pa));
+  cudaMemcpyToSymbol(c_pair_b, pb, sizeof(pb));
+  cudaMemcpyToSymbol(c_pair_idx, pidx, sizeof(pidx));
   done = true;
 }
 
@@ -256,8 +271,7 @@ __device__ __forceinline__ bool all_finite(const double (&P)[3][3], int vec) {
 // ------------------------------------------------------------- residual
 // 8 lanes per cell (lane q = quadrature point), 4 cells per warp.
 template <int MAT>
-__global__ void __launch_bounds__(kThreads) k_residual(ElemArgs a, const int32_t *__restrict__ list, int64_t n,
-                                                       double *__restrict__ R) {
+__global__ void __launch_bounds__(kThreads, 2) k_residual(ElemArgs a, int64_t n, double *__restrict__ Re) {
   constexpr int VEC = (MAT == B200FEM_MAT_POISSON) ? 1 : 3;
   __shared__ double sX[kWarps][4][8][3];
   __shared__ double sU[kWarps][4][8][VEC];
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(ElemArgs a, const int32_t
   for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
     const int64_t idx = base + slot;
     const bool valid = idx < n;
-    const int64_t e = list[valid ? idx : base];
+    const int64_t e = valid ? idx : base;
     const int node = a.cells[e * 8 + q];
 #pragma unroll
     for (int d = 0; d < 3; ++d) sX[w][slot][q][d] = a.coords[(int64_t)node * 3 + d];
@@ -318,11 +332,33 @@ __global__ void __launch_bounds__(kThreads) k_residual(ElemArgs a, const int32_t
     }
     double mine[VEC];
     reduce_scatter8<VEC>(r, q, mine);
-    if (valid) {
+    if (valid) {  // element block R_e[e, q, :] (node q of the cell), coalesced per cell
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) R[(int64_t)node * VEC + v] += mine[v];
+      for (int v = 0; v < VEC; ++v) Re[(e * 8 + q) * VEC + v] = mine[v];
     }
     __syncwarp();
+  }
+}
+
+// Ordered gather (assembly.py:256 semantics): R[n] = sum over the node's incident cells in
+// ascending cell id of R_e[e, a(n,e)] -- the reference's accumulation order, no atomics.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_residual_gather(const int32_t *__restrict__ n2c_ptr,
+                                                              const int32_t *__restrict__ n2c,
+                                                              const uint8_t *__restrict__ n2c_a,
+                                                              const double *__restrict__ Re, int64_t n_nodes,
+                                                              double s, const double *__restrict__ fN,
+                                                              const double *__restrict__ fB, double *__restrict__ R) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_nodes * VEC;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / VEC;
+    const int v = (int)(t - n * VEC);
+    double acc = 0.0;
+    for (int k = __ldg(n2c_ptr + n), k1 = __ldg(n2c_ptr + n + 1); k < k1; ++k)
+      acc += __ldg(Re + ((int64_t)__ldg(n2c + k) * 8 + __ldg(n2c_a + k)) * VEC + v);
+    if (fN) acc -= s * fN[t];
+    if (fB) acc -= fB[t];
+    R[t] = acc;
   }
 }
 
@@ -345,14 +381,20 @@ __global__ void k_res_dirichlet(double *__restrict__ R, const double *__restrict
 }
 
 // ------------------------------------------------------------- jacobian
-// Warp per cell.  Lanes 0..7 tabulate per-quadrature-point vectors in shared memory:
-//   g_k = G_k, u_k = F g_k, h_k = H g_k (NH) or s g_k (J2), and the scalar coefficients
-// of the closed-form block
-//   K_ik(a,b) = sum_q [ C1 d_ik (g_a.g_b) + Cl g_a,i g_b,k + Cm g_a,k g_b,i
-//                       - C2 (u_a,i h_b,k + h_a,i u_b,k) + C3 h_a,i h_b,k + C4 h_b,i h_a,k ]
-// (LE: C1=Cm=mu, Cl=lam; J2: C1=Cm=mu-beta/2, Cl=lam+beta/3, C3=-gamma;
-//  NH: C1=G a, C2=2/3 G a, C3=2/9 G a I1 + k(2J^2-J), C4=G/3 a I1 - k(J^2-J); all * JxW * theta^p)
-// then all 32 lanes accumulate two (a,b) 3x3 blocks each and RMW them into the CSR values.
+// Phase A, warp per cell.  Phase 1 uses all 32 lanes: lane (q, part) = (lane>>2, lane&3)
+// owns quadrature point q and nodes {part, part+4}; J and grad u are reduced over the 4
+// lanes of a point with shuffles, and each lane tabulates its two nodes' vectors in shared
+// memory.  The tangent block of pair (a,b) at a point is written in a factored form with
+// one FMA per term (coefficients include JxW and theta^p):
+//   NH:  K_ik += c1 d_ik (g_a.g_b) + h_a,i w_b,k + z_a,i h_b,k + t_b,i h_a,k
+//        h = H g, w = c3 h - c2 F g, z = -c2 F g, t = c4 h,
+//        c1 = G a, c2 = 2/3 G a, c3 = 2/9 G a I1 + k J(2J-1), c4 = G/3 a I1 - k J(J-1)
+//   J2:  K_ik += c1 d_ik (g_a.g_b) + cl g_a,i g_b,k + cm g_a,k g_b,i + y_a,i (c3 y_b,k),  y = s g
+//        c1 = cm = mu - beta/2, cl = lam + beta/3, c3 = -gamma
+//   LE:  J2 with beta = gamma = 0;   Poisson: alpha JxW (g_a.g_b)
+// (the algebra of SURVEY.md Appendix A; NH/J2 verified against the reference's AD Jacobian).
+// Phase 2: lane p computes the symmetric pair p of the 36 pairs a <= b over the 8 points and
+// writes the 3x3 block to the per-cell scratch.
 constexpr int kJacWarps = 4;
 
 template <int MAT>
@@ -360,61 +402,82 @@ struct JacSmem {
   double X[8][3];
   double U[8][3];
   double g[8][8][3];
-  double u[(MAT == B200FEM_MAT_NH) ? 8 : 1][8][3];
-  double h[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][8][3];
-  double coef[8][6];
-  int node[8];
+  double h[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][8][3];  // NH: H g; J2: c3 * s g
+  double w[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][8][3];  // NH: c3 h - c2 u; J2: s g
+  double z[(MAT == B200FEM_MAT_NH) ? 8 : 1][8][3];
+  double t[(MAT == B200FEM_MAT_NH) ? 8 : 1][8][3];
+  double coef[8][3];  // c1, cl, cm
 };
 
+__device__ __forceinline__ double quad_sum(double v) {  // sum over the 4 lanes of a point
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
 template <int MAT>
-__global__ void __launch_bounds__(kJacWarps * 32) k_jacobian(ElemArgs a, const int32_t *__restrict__ list, int64_t n,
-                                                             const uint8_t *__restrict__ cpos,
-                                                             const int32_t *__restrict__ indptr,
-                                                             double *__restrict__ data) {
+__global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int64_t n, double *__restrict__ Ke) {
   constexpr int VEC = (MAT == B200FEM_MAT_POISSON) ? 1 : 3;
   __shared__ JacSmem<MAT> sm_all[kJacWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   JacSmem<MAT> &S = sm_all[w];
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t idx = warp0; idx < n; idx += nwarps) {
-    const int64_t e = list[idx];
+  const int q = lane >> 2, part = lane & 3;
+  for (int64_t e = warp0; e < n; e += nwarps) {
     if (lane < 8) {
       const int node = a.cells[e * 8 + lane];
-      S.node[lane] = node;
 #pragma unroll
       for (int d = 0; d < 3; ++d) S.X[lane][d] = a.coords[(int64_t)node * 3 + d];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) S.U[lane][v] = a.U[(int64_t)node * VEC + v];
     }
     __syncwarp();
-    if (lane < 8) {
-      const int q = lane;
-      double G[8][3];
-      const double jxw = qp_geometry(S.X, q, G);
+    {  // ---- phase 1
+      double Jm[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double pj = S.X[part][i] * c_dN[q][part][j] + S.X[part + 4][i] * c_dN[q][part + 4][j];
+          Jm[i][j] = quad_sum(pj);
+        }
+      const double A0 = Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1], B0 = Jm[0][2] * Jm[2][1] - Jm[0][1] * Jm[2][2];
+      const double C0 = Jm[0][1] * Jm[1][2] - Jm[0][2] * Jm[1][1], D0 = Jm[1][2] * Jm[2][0] - Jm[1][0] * Jm[2][2];
+      const double E0 = Jm[0][0] * Jm[2][2] - Jm[0][2] * Jm[2][0], F0 = Jm[0][2] * Jm[1][0] - Jm[0][0] * Jm[1][2];
+      const double G0 = Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0], H0 = Jm[0][1] * Jm[2][0] - Jm[0][0] * Jm[2][1];
+      const double I0 = Jm[0][0] * Jm[1][1] - Jm[0][1] * Jm[1][0];
+      const double jxw = Jm[0][0] * A0 + Jm[0][1] * D0 + Jm[0][2] * G0;
+      const double r = 1.0 / jxw;
+      const double inv[3][3] = {{A0 * r, B0 * r, C0 * r}, {D0 * r, E0 * r, F0 * r}, {G0 * r, H0 * r, I0 * r}};
       double scale = jxw;
       if (a.mp.simp) scale *= pow(a.theta[e], a.mp.penalty);
+      double Gk[2][3];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int t = 0; t < 2; ++t) {
+        const int k = part + 4 * t;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) S.g[q][k][d] = G[k][d];
-      double C[6] = {0, 0, 0, 0, 0, 0};  // C1, Cl, Cm, C2, C3, C4
-      bool bad_def = false;
+        for (int aa = 0; aa < 3; ++aa)
+          Gk[t][aa] = inv[0][aa] * c_dN[q][k][0] + inv[1][aa] * c_dN[q][k][1] + inv[2][aa] * c_dN[q][k][2];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) S.g[q][k][d] = Gk[t][d];
+      }
+      bool bad_def = false, fin = true;
       double detF = 1.0;
       if (MAT == B200FEM_MAT_POISSON) {
-        C[0] = a.mp.alpha * scale;
+        if (part == 0) S.coef[q][0] = a.mp.alpha * scale;
       } else {
-        double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        double gu[3][3];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int v = 0; v < 3; ++v)
 #pragma unroll
-          for (int v = 0; v < 3; ++v)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) gu[v][d] = fma(S.U[k][v], G[k][d], gu[v][d]);
+          for (int d = 0; d < 3; ++d) gu[v][d] = quad_sum(S.U[part][v] * Gk[0][d] + S.U[part + 4][v] * Gk[1][d]);
         if (MAT == B200FEM_MAT_LE) {
-          C[0] = a.mp.mu * scale;
-          C[1] = a.mp.lam * scale;
-          C[2] = a.mp.mu * scale;
+          if (part == 0) {
+            S.coef[q][0] = a.mp.mu * scale;
+            S.coef[q][1] = a.mp.lam * scale;
+            S.coef[q][2] = a.mp.mu * scale;
+          }
         } else if (MAT == B200FEM_MAT_NH) {
           double F[3][3];
 #pragma unroll
@@ -440,126 +503,185 @@ __global__ void __launch_bounds__(kJacWarps * 32) k_jacobian(ElemArgs a, const i
             for (int j = 0; j < 3; ++j) I1 += F[i][j] * F[i][j];
           const double aa = bad_def ? 0.0 : pow(J, -2.0 / 3.0);
           const double Ga = a.mp.mu * aa;
-          C[0] = Ga * scale;
-          C[3] = (2.0 / 3.0) * Ga * scale;
-          C[4] = ((2.0 / 9.0) * Ga * I1 + a.mp.kappa * J * (2.0 * J - 1.0)) * scale;
-          C[5] = ((1.0 / 3.0) * Ga * I1 - a.mp.kappa * J * (J - 1.0)) * scale;
+          const double c1 = Ga * scale, c2 = (2.0 / 3.0) * Ga * scale;
+          const double c3 = ((2.0 / 9.0) * Ga * I1 + a.mp.kappa * J * (2.0 * J - 1.0)) * scale;
+          const double c4 = ((1.0 / 3.0) * Ga * I1 - a.mp.kappa * J * (J - 1.0)) * scale;
+          fin = isfinite(c1) && isfinite(c2) && isfinite(c3) && isfinite(c4);
+          if (part == 0) S.coef[q][0] = c1;
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
+          for (int t = 0; t < 2; ++t) {
+            const int k = part + 4 * t;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-              S.u[q][k][i] = F[i][0] * G[k][0] + F[i][1] * G[k][1] + F[i][2] * G[k][2];
-              S.h[q][k][i] = H[i][0] * G[k][0] + H[i][1] * G[k][1] + H[i][2] * G[k][2];
+              const double uk = F[i][0] * Gk[t][0] + F[i][1] * Gk[t][1] + F[i][2] * Gk[t][2];
+              const double hk = H[i][0] * Gk[t][0] + H[i][1] * Gk[t][1] + H[i][2] * Gk[t][2];
+              S.h[q][k][i] = hk;
+              S.w[q][k][i] = c3 * hk - c2 * uk;
+              S.z[q][k][i] = -c2 * uk;
+              S.t[q][k][i] = c4 * hk;
             }
+          }
         } else {  // J2 consistent tangent (derivative of j2_return_map incl. the s=0 guard)
           const double *ep = a.eps_prev + (e * 8 + q) * 9;
           const double *sp = a.sig_prev + (e * 8 + q) * 9;
-          double st[3][3], s[3][3], seff;
+          double st[3][3], sd[3][3], seff;
           bool pos;
-          j2_trial(gu, ep, sp, a.mp, st, s, seff, pos);
+          j2_trial(gu, ep, sp, a.mp, st, sd, seff, pos);
           const double over = fmax(seff - a.mp.sy, 0.0);
           const double f = over / seff;
           const double active = (seff - a.mp.sy > 0.0) ? 1.0 : 0.0;  // ramp'(0) = 0
           const double gam = pos ? (active / seff - over / (seff * seff)) * 3.0 * a.mp.mu / seff : 0.0;
           const double beta = 2.0 * a.mp.mu * f;
-          C[0] = (a.mp.mu - 0.5 * beta) * scale;
-          C[1] = (a.mp.lam + beta / 3.0) * scale;
-          C[2] = C[0];
-          C[4] = -gam * scale;
+          const double c1 = (a.mp.mu - 0.5 * beta) * scale, cl = (a.mp.lam + beta / 3.0) * scale;
+          const double c3 = -gam * scale;
+          fin = isfinite(c1) && isfinite(cl) && isfinite(c3);
+          if (part == 0) {
+            S.coef[q][0] = c1;
+            S.coef[q][1] = cl;
+            S.coef[q][2] = c1;
+          }
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
+          for (int t = 0; t < 2; ++t) {
+            const int k = part + 4 * t;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) S.h[q][k][i] = s[i][0] * G[k][0] + s[i][1] * G[k][1] + s[i][2] * G[k][2];
+            for (int i = 0; i < 3; ++i) {
+              const double y = sd[i][0] * Gk[t][0] + sd[i][1] * Gk[t][1] + sd[i][2] * Gk[t][2];
+              S.w[q][k][i] = y;
+              S.h[q][k][i] = c3 * y;
+            }
+          }
         }
       }
-      bool fin = true;
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        S.coef[q][j] = C[j];
-        fin &= isfinite(C[j]);
-      }
-      const unsigned long long key = (unsigned long long)e * 8 + q;
-      if (bad_def) {
-        atomicMin(&a.derr->inv_def, key);
-        atomicMin(&a.derr->min_detF, ord_bits(detF));
-      } else if (!fin) {
-        atomicMin(&a.derr->nonfin_d, key);
+      if (part == 0) {
+        const unsigned long long key = (unsigned long long)e * 8 + q;
+        if (bad_def) {
+          atomicMin(&a.derr->inv_def, key);
+          atomicMin(&a.derr->min_detF, ord_bits(detF));
+        } else if (!fin) {
+          atomicMin(&a.derr->nonfin_d, key);
+        }
       }
     }
     __syncwarp();
-    // ---- accumulate two (a,b) blocks per lane over the 8 quadrature points
-    const int b = lane & 7, a0 = lane >> 3, a1 = a0 + 4;
-    double K0[VEC][VEC], K1[VEC][VEC];
+    // ---- phase 2: the 36 symmetric pairs a <= b
+    for (int p = lane; p < 36; p += 32) {
+      const int a0 = c_pair_a[p], b = c_pair_b[p];
+      double K[VEC][VEC];
 #pragma unroll
-    for (int i = 0; i < VEC; ++i)
+      for (int i = 0; i < VEC; ++i)
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) K0[i][k] = K1[i][k] = 0.0;
+        for (int k = 0; k < VEC; ++k) K[i][k] = 0.0;
 #pragma unroll 2
-    for (int q = 0; q < 8; ++q) {
-      const double c1 = S.coef[q][0];
-      const double gb0 = S.g[q][b][0], gb1 = S.g[q][b][1], gb2 = S.g[q][b][2];
-      const double ga[2][3] = {{S.g[q][a0][0], S.g[q][a0][1], S.g[q][a0][2]},
-                               {S.g[q][a1][0], S.g[q][a1][1], S.g[q][a1][2]}};
-      const double gbv[3] = {gb0, gb1, gb2};
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double(&K)[VEC][VEC] = t ? K1 : K0;
-        const double gg = ga[t][0] * gb0 + ga[t][1] * gb1 + ga[t][2] * gb2;
+      for (int qq = 0; qq < 8; ++qq) {
+        const double ga[3] = {S.g[qq][a0][0], S.g[qq][a0][1], S.g[qq][a0][2]};
+        const double gb[3] = {S.g[qq][b][0], S.g[qq][b][1], S.g[qq][b][2]};
+        const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
+        const double d = S.coef[qq][0] * gg;
         if (MAT == B200FEM_MAT_POISSON) {
-          K[0][0] = fma(c1, gg, K[0][0]);
+          K[0][0] += d;
         } else {
-          const double d = c1 * gg;
 #pragma unroll
           for (int i = 0; i < 3; ++i) K[i][i] += d;
           if (MAT == B200FEM_MAT_LE || MAT == B200FEM_MAT_J2) {
-            const double cl = S.coef[q][1], cm = S.coef[q][2];
+            const double cl = S.coef[qq][1], cm = S.coef[qq][2];
+            double la[3], ma[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              la[i] = cl * ga[i];
+              ma[i] = cm * gb[i];
+            }
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
-              for (int k = 0; k < 3; ++k) K[i][k] += cl * ga[t][i] * gbv[k] + cm * ga[t][k] * gbv[i];
+              for (int k = 0; k < 3; ++k) K[i][k] = fma(la[i], gb[k], fma(ma[i], ga[k], K[i][k]));
           }
           if (MAT == B200FEM_MAT_J2) {
-            const double c3 = S.coef[q][4];
-            const int at = t ? a1 : a0;
-            const double ha[3] = {S.h[q][at][0], S.h[q][at][1], S.h[q][at][2]};
-            const double hb[3] = {S.h[q][b][0], S.h[q][b][1], S.h[q][b][2]};
+            const double ya[3] = {S.w[qq][a0][0], S.w[qq][a0][1], S.w[qq][a0][2]};
+            const double cyb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
-              for (int k = 0; k < 3; ++k) K[i][k] = fma(c3 * ha[i], hb[k], K[i][k]);
+              for (int k = 0; k < 3; ++k) K[i][k] = fma(ya[i], cyb[k], K[i][k]);
           }
           if (MAT == B200FEM_MAT_NH) {
-            const double c2 = S.coef[q][3], c3 = S.coef[q][4], c4 = S.coef[q][5];
-            const int at = t ? a1 : a0;
-            const double ha[3] = {S.h[q][at][0], S.h[q][at][1], S.h[q][at][2]};
-            const double hb[3] = {S.h[q][b][0], S.h[q][b][1], S.h[q][b][2]};
-            const double ua[3] = {S.u[q][at][0], S.u[q][at][1], S.u[q][at][2]};
-            const double ub[3] = {S.u[q][b][0], S.u[q][b][1], S.u[q][b][2]};
+            const double ha[3] = {S.h[qq][a0][0], S.h[qq][a0][1], S.h[qq][a0][2]};
+            const double hb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
+            const double wb[3] = {S.w[qq][b][0], S.w[qq][b][1], S.w[qq][b][2]};
+            const double za[3] = {S.z[qq][a0][0], S.z[qq][a0][1], S.z[qq][a0][2]};
+            const double tb[3] = {S.t[qq][b][0], S.t[qq][b][1], S.t[qq][b][2]};
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
-              for (int k = 0; k < 3; ++k)
-                K[i][k] += c3 * ha[i] * hb[k] + c4 * hb[i] * ha[k] - c2 * (ua[i] * hb[k] + ha[i] * ub[k]);
+              for (int k = 0; k < 3; ++k) K[i][k] = fma(ha[i], wb[k], fma(za[i], hb[k], fma(tb[i], ha[k], K[i][k])));
           }
         }
       }
+      double *out = Ke + (e * 36 + p) * (VEC * VEC);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) out[i * VEC + k] = K[i][k];
     }
-    // ---- scatter into the fixed CSR pattern (colour classes are node-disjoint)
-    const int nb = S.node[b];
-    (void)nb;
+    __syncwarp();
+  }
+}
+
+// Warp per node: the node's VEC rows (contiguous in the CSR values) are accumulated in
+// shared memory from its incident cells in ascending cell id -- every CSR slot sums its
+// contributions in the reference's order (assembly.py:296, kernels.py:30-34) -- then
+// Dirichlet rows become identity rows (assembly.py:297-299) and the block is written once.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_jacobian_gather(
+    const int32_t *__restrict__ n2c_ptr, const int32_t *__restrict__ n2c, const uint8_t *__restrict__ n2c_a,
+    const uint8_t *__restrict__ cpos, const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr,
+    const double *__restrict__ Ke, const uint8_t *__restrict__ dir_flag, int64_t n_nodes, int max_nbr,
+    double *__restrict__ data) {
+  extern __shared__ double gsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double *acc = gsm + (size_t)w * VEC * VEC * max_nbr;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = warp0; n < n_nodes; n += nwarps) {
+    const int p0 = __ldg(nbr_ptr + n), cnt = __ldg(nbr_ptr + n + 1) - p0;
+    const int L = VEC * cnt, T = VEC * L;
+    for (int t = lane; t < T; t += 32) acc[t] = 0.0;
+    __syncwarp();
+    const int k0 = __ldg(n2c_ptr + n), deg = __ldg(n2c_ptr + n + 1) - k0;
+    constexpr int ITEMS = 8 * VEC * VEC, PER = (ITEMS + 31) / 32;
+    for (int kc = 0; kc < deg; ++kc) {
+      const int64_t e = __ldg(n2c + k0 + kc);
+      const int a = __ldg(n2c_a + k0 + kc);
+      double v[PER];
+      int pos[PER];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int at = t ? a1 : a0;
-      const int na = S.node[at];
-      const int p = cpos[e * 64 + at * 8 + b];
-      double(&K)[VEC][VEC] = t ? K1 : K0;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        double *row = data + indptr[(int64_t)na * VEC + i] + VEC * p;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) row[k] += K[i][k];
+      for (int r = 0; r < PER; ++r) {  // the cell's loads are issued together
+        const int it = lane + 32 * r;
+        const bool ok = it < ITEMS;
+        const int b = it / (VEC * VEC), rr = it - b * VEC * VEC, i = rr / VEC, kk = rr - i * VEC;
+        const int pa = a <= b ? a : b, pb = a <= b ? b : a;
+        const int off = a <= b ? i * VEC + kk : kk * VEC + i;
+        v[r] = ok ? __ldg(Ke + (e * 36 + c_pair_idx[pa][pb]) * (VEC * VEC) + off) : 0.0;
+        pos[r] = ok ? i * L + VEC * __ldg(cpos + e * 64 + a * 8 + b) + kk : -1;
       }
+#pragma unroll
+      for (int r = 0; r < PER; ++r)
+        if (pos[r] >= 0) acc[pos[r]] += v[r];
+      __syncwarp();  // ascending cell order per slot
     }
+    if (dir_flag) {
+      int self = 0, hi = cnt;  // position of n in its own neighbour list
+      while (self < hi) {
+        const int mid = (self + hi) >> 1;
+        if (__ldg(nbr + p0 + mid) < (int)n) self = mid + 1; else hi = mid;
+      }
+      for (int i = 0; i < VEC; ++i) {
+        if (!__ldg(dir_flag + n * VEC + i)) continue;
+        for (int t = lane; t < L; t += 32) acc[i * L + t] = (t == VEC * self + i) ? 1.0 : 0.0;
+      }
+      __syncwarp();
+    }
+    double *out = data + (int64_t)VEC * VEC * p0;
+    for (int t = lane; t < T; t += 32) out[t] = acc[t];
     __syncwarp();
   }
 }
@@ -755,31 +877,39 @@ int fetch_element_errors(Ctx *c, b200fem_error *err, bool jacobian) {
   return code;
 }
 
-template <int MAT>
-static void residual_colors(Ctx *c, const ElemArgs &a, double *R) {
-  for (int col = 0; col < c->n_colors; ++col) {
-    const int64_t lo = c->color_off[col], n = c->color_off[col + 1] - lo;
-    if (n == 0) continue;
-    k_residual<MAT><<<grid_cap(n, kWarps * 4), kThreads, 0, c->stream>>>(a, c->color_cells + lo, n, R);
-    count_launch();
-  }
+static int ensure_scratch(Ctx *c, size_t len, b200fem_error *err) {
+  if (c->scratch_len >= len) return 0;
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_len = 0;
+  B200_CUDA_E(dalloc(&c->scratch, len), err);
+  c->scratch_len = len;
+  return 0;
 }
 
+// Two-phase residual: (1) per-cell blocks R_e (one launch over all cells), (2) ordered
+// per-node gather fused with the load subtraction; Dirichlet rows overwritten last.
 int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int apply_dirichlet, b200fem_error *err,
                     double *norm_host) {
   cudaStream_t s = c->stream;
-  B200_CUDA_E(cudaMemsetAsync(R, 0, c->n_dofs * sizeof(double), s), err);
+  if (ensure_scratch(c, (size_t)c->n_cells * 8 * c->vec, err)) return B200FEM_E_CUDA;
   const ElemArgs a = make_args(c, U);
+  const int g = grid_cap(c->n_cells, kWarps * 4);
   switch (c->material) {
-    case B200FEM_MAT_POISSON: residual_colors<B200FEM_MAT_POISSON>(c, a, R); break;
-    case B200FEM_MAT_LE: residual_colors<B200FEM_MAT_LE>(c, a, R); break;
-    case B200FEM_MAT_NH: residual_colors<B200FEM_MAT_NH>(c, a, R); break;
-    default: residual_colors<B200FEM_MAT_J2>(c, a, R); break;
+    case B200FEM_MAT_POISSON: k_residual<B200FEM_MAT_POISSON><<<g, kThreads, 0, s>>>(a, c->n_cells, c->scratch); break;
+    case B200FEM_MAT_LE: k_residual<B200FEM_MAT_LE><<<g, kThreads, 0, s>>>(a, c->n_cells, c->scratch); break;
+    case B200FEM_MAT_NH: k_residual<B200FEM_MAT_NH><<<g, kThreads, 0, s>>>(a, c->n_cells, c->scratch); break;
+    default: k_residual<B200FEM_MAT_J2><<<g, kThreads, 0, s>>>(a, c->n_cells, c->scratch); break;
   }
-  if (c->f_neumann || c->f_body) {
-    k_res_finalize<<<grid_cap(c->n_dofs, kThreads), kThreads, 0, s>>>(R, c->n_dofs, bc_scale, c->f_neumann, c->f_body);
-    count_launch();
-  }
+  const int gg = grid_cap(c->n_dofs, kThreads);
+  if (c->vec == 3)
+    k_residual_gather<3><<<gg, kThreads, 0, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->scratch, c->n_nodes, bc_scale,
+                                                 c->f_neumann, c->f_body, R);
+  else
+    k_residual_gather<1><<<gg, kThreads, 0, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->scratch, c->n_nodes, bc_scale,
+                                                 c->f_neumann, c->f_body, R);
+  count_launch(2);
   if (apply_dirichlet && c->n_dir) {
     k_res_dirichlet<<<grid_cap(c->n_dir, kThreads), kThreads, 0, s>>>(R, U, c->dir_dofs, c->dir_vals, c->n_dir,
                                                                       bc_scale);
@@ -796,32 +926,36 @@ int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int app
   return 0;
 }
 
-template <int MAT>
-static void jacobian_colors(Ctx *c, const ElemArgs &a, double *data) {
-  for (int col = 0; col < c->n_colors; ++col) {
-    const int64_t lo = c->color_off[col], n = c->color_off[col + 1] - lo;
-    if (n == 0) continue;
-    k_jacobian<MAT><<<grid_cap(n, kJacWarps), kJacWarps * 32, 0, c->stream>>>(a, c->color_cells + lo, n, c->cpos,
-                                                                               c->indptr, data);
-    count_launch();
-  }
-}
-
+// Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
+// (2) warp-per-node ordered gather writing each CSR row segment exactly once.
 int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err) {
   cudaStream_t s = c->stream;
-  B200_CUDA_E(cudaMemsetAsync(data, 0, c->nnz * sizeof(double), s), err);
+  const int vv = c->vec * c->vec;
+  if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
   const ElemArgs a = make_args(c, U);
+  const int g = grid_cap(c->n_cells, kJacWarps);
   switch (c->material) {
-    case B200FEM_MAT_POISSON: jacobian_colors<B200FEM_MAT_POISSON>(c, a, data); break;
-    case B200FEM_MAT_LE: jacobian_colors<B200FEM_MAT_LE>(c, a, data); break;
-    case B200FEM_MAT_NH: jacobian_colors<B200FEM_MAT_NH>(c, a, data); break;
-    default: jacobian_colors<B200FEM_MAT_J2>(c, a, data); break;
+    case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
+    case B200FEM_MAT_LE: k_jacobian<B200FEM_MAT_LE><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
+    case B200FEM_MAT_NH: k_jacobian<B200FEM_MAT_NH><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
+    default: k_jacobian<B200FEM_MAT_J2><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
   }
-  if (c->n_dir) {
-    k_jac_dirichlet<<<grid_cap(c->n_dir * 32, kThreads), kThreads, 0, s>>>(data, c->indptr, c->diag, c->dir_dofs,
-                                                                           c->n_dir);
-    count_launch();
+  int warps = 8;
+  while (warps > 1 && (size_t)warps * vv * c->max_nbr * sizeof(double) > 96 * 1024) warps >>= 1;
+  const size_t smem = (size_t)warps * vv * c->max_nbr * sizeof(double);
+  const int gg = grid_cap(c->n_nodes, warps);
+  if (c->vec == 3) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_jacobian_gather<3><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
+                                                     c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
+                                                     c->max_nbr, data);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_jacobian_gather<1><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
+                                                     c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
+                                                     c->max_nbr, data);
   }
+  count_launch(2);
   B200_CUDA_E(cudaGetLastError(), err);
   return fetch_element_errors(c, err, true);
 }

@@ -93,6 +93,13 @@ struct Ctx {
   uint8_t *cpos = nullptr;    // (n_cells,64) position of node b in node a's neighbour list
   int32_t *diag = nullptr;    // (n_dofs) diagonal slot
   int max_nbr = 0;
+  int max_deg = 0;              // max cells per node
+  int32_t *n2c_ptr = nullptr;   // (n_nodes+1) node -> incident cells, ascending cell id
+  int32_t *n2c = nullptr;
+  uint8_t *n2c_a = nullptr;     // local index (0..7) of the node in each incident cell
+  uint8_t *dir_flag = nullptr;  // (n_dofs) 1 on Dirichlet rows
+  double *scratch = nullptr;    // per-cell element blocks (two-phase assembly)
+  size_t scratch_len = 0;
   // colouring (host offsets, device cell lists ordered by colour then cell id)
   int n_colors = 0;
   std::vector<int64_t> color_off;
@@ -138,6 +145,10 @@ struct Matrix {
   bool use_tma = false;
   // rows computed by matvec/Krylov: node range (FEM3) or row range (CSR); -1 = all
   int64_t row_lo = 0, row_hi = -1;
+  // Dirichlet identity rows (FEM matrices): PCG starts from x_d = b_d so that the Krylov
+  // space stays in {v : v_d = 0}, where the row-replaced K acts as the SPD block K_ff
+  const int32_t *dir_dofs = nullptr;
+  int64_t n_dir = 0;
 };
 
 // allocation helpers
@@ -156,7 +167,7 @@ int launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s)
 int launch_scale(int64_t n, double a, const double *x, double *y, cudaStream_t s);
 
 // sparse
-enum SpmvMode : int { SP_PLAIN = 0, SP_JACOBI_R0 = 1, SP_JACOBI_TT = 2, SP_RESIDUAL = 3 };
+enum SpmvMode : int { SP_PLAIN = 0, SP_JACOBI_R0 = 1, SP_JACOBI_TT = 2, SP_RESIDUAL = 3, SP_PQ = 4, SP_CGRES = 5 };
 struct SpmvArgs {
   const double *x;   // operand (p, s or x)
   double *y;         // output (v, t or r)
@@ -218,7 +229,7 @@ __device__ __forceinline__ void iter_start(KrylovScalars *S) {
   S->rho = rho_new;
 }
 
-enum StageKind : int { ST_R0 = 1, ST_TT = 2, ST_RES = 3, ST_XR = 4 };
+enum StageKind : int { ST_R0 = 1, ST_TT = 2, ST_RES = 3, ST_XR = 4, ST_PQ = 5, ST_CGRES = 6, ST_CGXR = 7 };
 // Scalar update after a reduction with global totals tot[] (solvers.py:141-167).
 __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const double *tot) {
   if (!S || S->status != KS_RUNNING) return;
@@ -236,7 +247,7 @@ __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const do
     S->mv += 1;
     S->res = sqrt(tot[0]);
     S->r0r0 = S->r0r = S->rr = tot[1];
-  } else {  // ST_XR
+  } else if (kind == ST_XR) {
     S->res = sqrt(tot[0]);
     S->r0r = tot[1];
     S->rr = tot[2];
@@ -245,6 +256,28 @@ __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const do
       return;
     }
     iter_start(S);
+  } else if (kind == ST_PQ) {  // Jacobi-PCG: alpha = (r.z) / (p.Ap); p.Ap <= 0 -> not SPD
+    S->mv += 1;
+    S->r0v = tot[0];
+    if (!(tot[0] > 0.0)) S->status = KS_BREAKDOWN;
+    else S->alpha = S->rho / tot[0];
+  } else if (kind == ST_CGRES) {  // explicit residual: ||r||, r.z (p = z)
+    S->mv += 1;
+    S->res = sqrt(tot[0]);
+    S->rho = tot[1];
+  } else {  // ST_CGXR: after x += alpha p, r -= alpha q, z = D^-1 r
+    S->res = sqrt(tot[0]);
+    if (S->res <= S->tol) {
+      S->status = KS_CONV_INNER;
+      return;
+    }
+    if (S->it >= S->max_iters) {
+      S->status = KS_MAXED;
+      return;
+    }
+    S->it += 1;
+    S->beta = tot[1] / S->rho;
+    S->rho = tot[1];
   }
 }
 

@@ -24,6 +24,12 @@
 
 namespace b200 {
 
+__global__ void k_begin_cg(KrylovScalars *S) {
+  if (S->status != KS_RUNNING) return;
+  if (S->it >= S->max_iters) S->status = KS_MAXED;
+  else S->it += 1;
+}
+
 __global__ void k_begin(KrylovScalars *S) {
   if (S->status == KS_RUNNING) iter_start(S);
 }
@@ -65,6 +71,45 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
   }
   double tot[3];
   if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0 && inline_stage) apply_stage(ST_XR, S, tot);
+}
+
+// ---------------------------------------------------------------- Jacobi-PCG
+// For symmetric operators (Poisson, LE, NH, SIMP, J2 tangents; BASELINE config 2 "linear
+// assembly + PCG").  The Dirichlet rows of the assembled K are identity rows, so starting
+// from x_d = b_d keeps r_d = z_d = p_d = 0 and the row-replaced K acts on the Krylov space
+// as the SPD block K_ff (the lifting K_fd x_d enters through the first residual).
+__global__ void k_set_dirichlet(double *__restrict__ x, const double *__restrict__ b, const int32_t *__restrict__ d,
+                                int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[d[i]] = b[d[i]];
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_update_xrz(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                                                            const double *__restrict__ p, const double *__restrict__ q,
+                                                            const double *__restrict__ inv, double *__restrict__ z,
+                                                            KrylovScalars *S, RedScratch red, int inline_stage) {
+  if (S->status != KS_RUNNING) return;
+  const double alpha = S->alpha;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    const double zi = inv[i] * ri;
+    z[i] = zi;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(ri, zi, acc[1]);
+  }
+  double tot[2];
+  if (block_partials_and_finish<2>(acc, red, tot) && threadIdx.x == 0 && inline_stage) apply_stage(ST_CGXR, S, tot);
+}
+
+__global__ void __launch_bounds__(kThreads) k_cg_update_p(int64_t n, const double *__restrict__ z,
+                                                          double *__restrict__ p, const KrylovScalars *S) {
+  if (S->status != KS_RUNNING) return;
+  const double beta = S->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
 }
 
 int ensure_work(Matrix *m) {
@@ -221,6 +266,109 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
   }
 }
 
+static void enqueue_cg_iteration(Matrix *m, double *x) {
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  const int64_t n = m->n;
+  SpmvArgs a{w->p, w->v, w->inv, w->diag, nullptr, nullptr, w->sc, 1};
+  launch_spmv(m, SP_PQ, a, &w->red);
+  k_cg_update_xrz<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->v, w->inv, w->s, w->sc, w->red, 1);
+  k_cg_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->s, w->p, w->sc);
+  count_launch(2);
+}
+
+int pcg(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol, int64_t max_iters,
+        b200fem_solve_info *info, b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  if (info) memset(info, 0, sizeof(*info));
+  if (!(rel_tol > 0) || !(abs_tol > 0)) {
+    set_err(err, B200FEM_E_INVALID, "linear solver tolerances must be positive");
+    return B200FEM_E_INVALID;
+  }
+  int st = ensure_work(m);
+  if (st) return set_err(err, st, "Krylov workspace allocation failed"), st;
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  const int64_t n = m->n;
+  int64_t nzero = 0;
+  st = launch_diagonal(m, w->diag, w->inv, &w->red, &nzero);
+  if (st) return set_err(err, st, "diagonal extraction failed"), st;
+  if (nzero) {
+    set_err(err, B200FEM_E_ZERO_DIAGONAL, "zero diagonal entry; Jacobi preconditioner undefined");
+    return B200FEM_E_ZERO_DIAGONAL;
+  }
+  if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x, 0, n * sizeof(double), s), err);
+  if (m->n_dir) {
+    k_set_dirichlet<<<grid_vec(m->n_dir), kThreads, 0, s>>>(x, b, m->dir_dofs, m->n_dir);
+    count_launch();
+  }
+  if (launch_dot(b, b, n, &w->red, s)) return B200FEM_E_CUDA;
+  double bb = 0.0;
+  B200_CUDA_E(cudaMemcpyAsync(&bb, w->red.result, sizeof(double), cudaMemcpyDeviceToHost, s), err);
+  B200_CUDA_E(cudaStreamSynchronize(s), err);
+  const double tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
+  const int64_t max_it = max_iters > 0 ? max_iters : 10 * n;
+  KrylovScalars *H = w->sc_host;
+  memset(H, 0, 3 * sizeof(KrylovScalars));
+  H[0].tol = tol;
+  H[0].max_iters = max_it;
+  long long it = 0, mv = 0, restarts = 0;
+  const size_t ssz = sizeof(KrylovScalars);
+  for (;;) {
+    H[0].status = KS_RUNNING;
+    H[0].it = it;
+    H[0].mv = mv;
+    B200_CUDA_E(cudaMemcpyAsync(w->sc, &H[0], ssz, cudaMemcpyHostToDevice, s), err);
+    SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->p, w->sc, 1};  // r = b - A x, p = D^-1 r
+    if (launch_spmv(m, SP_CGRES, ar, &w->red)) return B200FEM_E_CUDA;
+    ++restarts;
+    B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+    B200_CUDA_E(cudaStreamSynchronize(s), err);
+    mv = H[1].mv;
+    const double res = H[1].res;
+    if (res <= tol) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      return 0;
+    }
+    if (it >= max_it) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      if (err) err->iterations = it, err->value = res;
+      set_err(err, B200FEM_E_LINEAR_SOLVER, "PCG did not converge in %lld iterations (residual %.3e, tol %.3e)",
+              (long long)max_it, res, tol);
+      return B200FEM_E_LINEAR_SOLVER;
+    }
+    k_begin_cg<<<1, 1, 0, s>>>(w->sc);
+    count_launch();
+    int batch = 4, cur = 0;
+    auto enqueue_batch = [&](int slot) -> int {
+      for (int i = 0; i < batch; ++i) enqueue_cg_iteration(m, x);
+      B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+      B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
+      return 0;
+    };
+    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
+    for (;;) {
+      batch = std::min(batch * 2, 32);
+      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
+      B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
+      if (H[1 + cur].status != KS_RUNNING) break;
+      cur ^= 1;
+    }
+    B200_CUDA_E(cudaStreamSynchronize(s), err);
+    const KrylovScalars done = H[1 + (cur ^ 1)];
+    it = done.it;
+    mv = done.mv;
+    B200_CUDA_E(cudaGetLastError(), err);
+    if (done.status == KS_BREAKDOWN) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, done.res, tol};
+      if (err) err->iterations = it, err->value = done.res;
+      set_err(err, B200FEM_E_BREAKDOWN, "PCG breakdown at iteration %lld: p.Ap = %.3e <= 0 (operator not SPD)", it,
+              done.r0v);
+      return B200FEM_E_BREAKDOWN;
+    }
+  }
+}
+
 }  // namespace b200
 
 using namespace b200;
@@ -236,6 +384,8 @@ int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *dat
   m->data = data;
   m->stream = c->stream;
   m->diag_slots = c->diag;
+  m->dir_dofs = c->dir_dofs;
+  m->n_dir = c->n_dir;
   if (c->vec == 3) {
     m->kind = MK_FEM3;
     m->nbr_ptr = c->nbr_ptr;
@@ -306,6 +456,16 @@ int b200fem_diagonal(b200fem_matrix *mm, double *diag) {
   if (st) return st;
   st = launch_diagonal(m, diag, m->kw->inv, &m->kw->red, nullptr);
   return st;
+}
+
+int b200fem_pcg(b200fem_matrix *mm, const double *b, double *x, int32_t has_x0, double rel_tol, double abs_tol,
+                int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+  Matrix *m = (Matrix *)mm;
+  if (m->n == 0) {
+    if (info) memset(info, 0, sizeof(*info));
+    return 0;
+  }
+  return pcg(m, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
 }
 
 int b200fem_bicgstab(b200fem_matrix *mm, const double *b, double *x, int32_t has_x0, double rel_tol, double abs_tol,

@@ -42,6 +42,11 @@ __device__ __forceinline__ RowPre spmv_preload(int64_t i, const SpmvArgs &a) {
     p.inv = __ldg(a.inv + i);
     p.aux = __ldg(a.aux + i);
     p.dg = __ldg(a.dg + i);
+  } else if (MODE == SP_PQ) {
+    p.xi = __ldg(a.x + i);
+  } else if (MODE == SP_CGRES) {
+    p.inv = __ldg(a.inv + i);
+    p.aux = __ldg(a.aux + i);
   }
   return p;
 }
@@ -61,13 +66,23 @@ __device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvA
     a.y[i] = t;
     red0 = fma(t, t, red0);
     red1 = fma(t, p.xi, red1);
-  } else {  // SP_RESIDUAL
+  } else if (MODE == SP_RESIDUAL) {
     const double r = p.inv * (p.aux - acc);
     a.y[i] = r;
     a.aux2[i] = r;
     const double dr = p.dg * r;
     red0 = fma(dr, dr, red0);
     red1 = fma(r, r, red1);
+  } else if (MODE == SP_PQ) {  // q = A p, p.q
+    a.y[i] = acc;
+    red0 = fma(p.xi, acc, red0);
+  } else {  // SP_CGRES: r = b - A x, p = z = D^-1 r, ||r||^2, r.z
+    const double r = p.aux - acc;
+    const double z = p.inv * r;
+    a.y[i] = r;
+    a.aux2[i] = z;
+    red0 = fma(r, r, red0);
+    red1 = fma(r, z, red1);
   }
 }
 
@@ -77,6 +92,8 @@ __device__ __forceinline__ void spmv_stage(KrylovScalars *S, const double (&tot)
   if (MODE == SP_JACOBI_R0) apply_stage(ST_R0, S, tot);
   else if (MODE == SP_JACOBI_TT) apply_stage(ST_TT, S, tot);
   else if (MODE == SP_RESIDUAL) apply_stage(ST_RES, S, tot);
+  else if (MODE == SP_PQ) apply_stage(ST_PQ, S, tot);
+  else if (MODE == SP_CGRES) apply_stage(ST_CGRES, S, tot);
 }
 
 // Sum three per-lane partials over the warp with a reduce-scatter (6 double shuffles
@@ -332,6 +349,8 @@ int prepare_fem3_chunks(Matrix *m) {
     cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     cudaFuncSetAttribute(k_spmv_fem3_tma<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_CGRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
     attr = true;
   }
   m->use_tma = true;
@@ -412,6 +431,8 @@ int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *r
     case SP_PLAIN: spmv_dispatch<SP_PLAIN>(m, a, red); break;
     case SP_JACOBI_R0: spmv_dispatch<SP_JACOBI_R0>(m, a, red); break;
     case SP_JACOBI_TT: spmv_dispatch<SP_JACOBI_TT>(m, a, red); break;
+    case SP_PQ: spmv_dispatch<SP_PQ>(m, a, red); break;
+    case SP_CGRES: spmv_dispatch<SP_CGRES>(m, a, red); break;
     default: spmv_dispatch<SP_RESIDUAL>(m, a, red); break;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;

@@ -23,7 +23,7 @@ from .mesh import BoundaryLocator, locate_nodes
 from .sparse import CsrMatrix
 
 __all__ = ["LinearSolveConfig", "NewtonConfig", "LoadSchedule", "LinearSolverError", "BreakdownError",
-           "NonConvergenceError", "bicgstab_jacobi", "newton_solve", "incremental_solve", "reaction_force",
+           "NonConvergenceError", "bicgstab_jacobi", "pcg_jacobi", "newton_solve", "incremental_solve", "reaction_force",
            "quad_point_stress", "volume_averaged_stress", "NewtonReport", "StepRecord", "LoadHistory"]
 
 
@@ -32,10 +32,15 @@ class LinearSolveConfig:
     rel_tol: float = 1e-10
     abs_tol: float = 1e-12
     max_iters: int = 0  # 0 -> 10 * N
+    # "bicgstab" = the reference solver (solvers.py:87-167, default); "pcg" = Jacobi-CG for
+    # symmetric tangents (north_star "CG/BiCGSTAB", BASELINE config 2), same stopping rule
+    method: str = "bicgstab"
 
     def __post_init__(self):
         if self.rel_tol <= 0 or self.abs_tol <= 0:
             raise ValueError("linear solver tolerances must be positive")
+        if self.method not in ("bicgstab", "pcg"):
+            raise ValueError(f"unknown linear solver {self.method!r}")
 
 
 @dataclass(frozen=True)
@@ -82,12 +87,14 @@ class SolveStats:
     tol: float = 0.0
 
 
-def _bicgstab_device(A: CsrMatrix, b, x, has_x0: bool, cfg: LinearSolveConfig) -> SolveStats:
+def _bicgstab_device(A: CsrMatrix, b, x, has_x0: bool, cfg: LinearSolveConfig, method=None) -> SolveStats:
     info = _lib.SolveInfo()
     err = _lib.Error()
-    st = _lib.lib().b200fem_bicgstab(A._device_handle(), D.ptr(b), D.ptr(x), int(has_x0), float(cfg.rel_tol),
-                                     float(cfg.abs_tol), int(cfg.max_iters), C.byref(info), C.byref(err))
-    raise_for(st, err, "bicgstab")
+    method = method or cfg.method
+    fn = _lib.lib().b200fem_pcg if method == "pcg" else _lib.lib().b200fem_bicgstab
+    st = fn(A._device_handle(), D.ptr(b), D.ptr(x), int(has_x0), float(cfg.rel_tol), float(cfg.abs_tol),
+            int(cfg.max_iters), C.byref(info), C.byref(err))
+    raise_for(st, err, method)
     return SolveStats(info.iterations, info.matvecs, info.restarts, info.residual, info.tol)
 
 
@@ -102,7 +109,23 @@ def bicgstab_jacobi(A: CsrMatrix, b, x0=None, cfg: LinearSolveConfig = LinearSol
     if tuple(bd.shape) != (n,):
         raise ValueError(f"b must have shape ({n},), got {tuple(bd.shape)}")
     x = D.zeros(n) if x0 is None else D.to_device(x0, copy=True)
-    s = _bicgstab_device(A, bd, x, x0 is not None, cfg)
+    s = _bicgstab_device(A, bd, x, x0 is not None, cfg, method="bicgstab")
+    if stats is not None:
+        stats.append(s)
+    return D.to_host(x) if as_host else x
+
+
+def pcg_jacobi(A: CsrMatrix, b, x0=None, cfg: LinearSolveConfig = LinearSolveConfig(), stats=None):
+    """Solve A x = b by Jacobi-preconditioned CG on the GPU (symmetric A; FEM matrices with
+    Dirichlet identity rows are handled by starting from x_d = b_d).  Same termination rule
+    and exceptions as bicgstab_jacobi; BreakdownError if A is found not positive definite."""
+    as_host = not D.is_device_tensor(b)
+    bd = D.to_device(b)
+    n = A.shape[0]
+    if tuple(bd.shape) != (n,):
+        raise ValueError(f"b must have shape ({n},), got {tuple(bd.shape)}")
+    x = D.zeros(n) if x0 is None else D.to_device(x0, copy=True)
+    s = _bicgstab_device(A, bd, x, x0 is not None, cfg, method="pcg")
     if stats is not None:
         stats.append(s)
     return D.to_host(x) if as_host else x

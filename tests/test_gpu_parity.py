@@ -349,3 +349,31 @@ def test_bulk_copy_spmv_bit_identical_to_ldg_kernel(rng, monkeypatch):
     cfg = fem.LinearSolveConfig(rel_tol=1e-12, abs_tol=1e-14)
     x1, x2 = fem.bicgstab_jacobi(K2, b, cfg=cfg), fem.bicgstab_jacobi(K, b, cfg=cfg)
     assert rel(x1, x2) < 1e-9
+
+
+# ------------------------------------------------------------------ Jacobi-PCG
+def test_pcg_matches_dense_lu_with_dirichlet_rows(rng):
+    prob, A = _poisson_matrix(5)
+    b = rng.standard_normal(prob.n_dofs)
+    cfg = fem.LinearSolveConfig(rel_tol=1e-12, abs_tol=1e-14)
+    x = fem.pcg_jacobi(A, b, cfg=cfg)
+    x_lu = np.linalg.solve(A.todense(), b)
+    assert np.abs(x - x_lu).max() / np.abs(x_lu).max() < 1e-9
+    assert np.linalg.norm(A.todense() @ x - b) <= max(1e-12 * np.linalg.norm(b), 1e-14) * 1.0001
+    assert np.array_equal(fem.pcg_jacobi(A, np.zeros(prob.n_dofs)), np.zeros(prob.n_dofs))
+
+
+def test_pcg_breakdown_on_indefinite():
+    A = _dense_csr(np.array([[1.0, 2.0], [2.0, 1.0]]))  # eigenvalues 3, -1
+    with pytest.raises(fem.BreakdownError, match="not SPD"):
+        fem.pcg_jacobi(A, np.array([1.0, -1.0]))
+
+
+@pytest.mark.parametrize("name", ["c1", "nh_block", "simp", "poisson", "simp_nh", "le_body"])
+def test_newton_with_pcg_matches_reference(name):
+    g = load_golden(name)
+    _, prob, _ = build(name)
+    U, rep = fem.newton_solve(prob, cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11),
+                              lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method="pcg"))
+    assert rep.converged
+    assert rel(U, g["U_tight"]) < 1e-8
