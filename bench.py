@@ -43,6 +43,9 @@ def parse():
     p.add_argument("--stretch", type=float, default=0.02)
     p.add_argument("--cpu-sample-n", type=int, default=12)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--linear", default="bicgstab", choices=["bicgstab", "pcg"],
+                   help="Krylov method of the timed Newton solve (reference default: bicgstab)")
+    p.add_argument("--no-alt", action="store_true", help="skip the one-solve measurement of the other method")
     p.add_argument("--partitioned", action="store_true",
                    help="use the partitioned (multi-GPU) solver even on one rank (path check)")
     return p.parse_args()
@@ -223,17 +226,18 @@ def run_ours(args):
         fem.DirichletSpec(top, 2, lambda p, s=s: np.full(np.asarray(p).shape[:-1], s) if np.ndim(p) > 1 else s)]
     prob = fem.NeoHookeanProblem(mesh, alu, specs)
     N = prob.n_dofs
+    lin = fem.LinearSolveConfig(method=args.linear)
     t0 = time.perf_counter()
     if world == 1 and not args.partitioned:
         ws = fem.workspace(prob)
         U0 = D.zeros(N)
         sub, part = prob, None
 
-        def step():
-            return fem.newton_solve(prob, U0)
+        def step(lin=lin):
+            return fem.newton_solve(prob, U0, lin_cfg=lin)
 
         def e2e_step(U0_host):
-            U, _ = fem.newton_solve(prob, U0_host)  # pinned host in, numpy out
+            U, _ = fem.newton_solve(prob, U0_host, lin_cfg=lin)  # pinned host in, numpy out
             return U
     else:
         from paper_2212_00964_b200.distributed import PartitionedSolver
@@ -242,11 +246,11 @@ def run_ours(args):
         part = solver.parts[0]
         ws, sub = part.ws, part.problem
 
-        def step():
-            return None, solver.newton_solve()
+        def step(lin=lin):
+            return None, solver.newton_solve(lin_cfg=lin)
 
         def e2e_step(U0_host):
-            solver.newton_solve(U0_host)
+            solver.newton_solve(U0_host, lin_cfg=lin)
             lo, hi = part.own_dofs
             return D.to_host(part.U[lo:hi])
     torch.cuda.synchronize()
@@ -329,6 +333,20 @@ def run_ours(args):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     d2h = 8 * N if part is None else 8 * (part.own_dofs[1] - part.own_dofs[0])
 
+    # ---------------- the other Krylov method, one device-timed solve (same problem, same tolerances)
+    alt = None
+    if not args.no_alt and part is None:
+        other = "pcg" if args.linear == "bicgstab" else "bicgstab"
+        olin = fem.LinearSolveConfig(method=other)
+        barrier()
+        e0.record()
+        _, orep = step(olin)
+        e1.record()
+        torch.cuda.synchronize()
+        alt = {"method": other, "newton_s": e0.elapsed_time(e1) / 1e3, "newton_iterations": orep.n_iterations,
+               "linear_iterations": [s_.iterations for s_ in orep.linear_stats],
+               "matvecs": sum(s_.matvecs for s_ in orep.linear_stats), "residual_norms": orep.residual_norms}
+
     peak, peak_kind = peaks()
     traffic = ncu_traffic()
     achieved = bytes_fem / t_spmv / 1e9
@@ -345,8 +363,10 @@ def run_ours(args):
                      "frac": achieved / peak, "bytes_per_launch": bytes_fem,
                      "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,
                      "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6},
-        "newton": {"iterations": rep.n_iterations, "residual_norms": rep.residual_norms,
-                   "linear_iterations": lin_iters, "matvecs": matvecs, "per_step_ms": per_step},
+        "newton": {"linear_method": args.linear, "iterations": rep.n_iterations,
+                   "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
+                   "per_step_ms": per_step},
+        "alt_linear": alt,
         "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": n_cells_l / t_res / 1e6,
                      "jacobian_ms": t_jac * 1e3, "jacobian_mcells_s": n_cells_l / t_jac / 1e6,
                      "jacobian_hbm_gbs": (8 * ws.nnz + 32 * n_cells_l + 24 * n_nodes_l + 8 * Nl) / t_jac / 1e9,

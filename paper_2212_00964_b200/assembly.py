@@ -95,8 +95,14 @@ def _neumann_load(mesh: Mesh, vec: int, specs) -> np.ndarray:
         t = _eval_pointwise(spec.traction_fn, fq.points.reshape(-1, 3), (facets.shape[0] * 4, vec))
         fe = np.einsum("fqv,qa,fq->fav", t.reshape(-1, 4, vec), fq.shape_values, fq.JxW)
         dofs = mesh.cells[facets[:, 0][:, None], fq.local_nodes][:, :, None] * vec + np.arange(vec)
-        np.add.at(f, dofs.ravel(), fe.ravel())
+        f += _ordered_scatter(dofs.ravel(), fe.ravel(), f.size)
     return f
+
+
+def _ordered_scatter(idx, vals, n):
+    """sum_k vals[k] into out[idx[k]] in ascending k (same order as the reference's
+    sequential scatter_add, kernels.py:30-34); np.bincount accumulates in input order."""
+    return np.bincount(idx, weights=vals, minlength=n)
 
 
 def _body_load(mesh: Mesh, vec: int, body) -> np.ndarray:
@@ -107,8 +113,7 @@ def _body_load(mesh: Mesh, vec: int, body) -> np.ndarray:
     b = _eval_pointwise(body, xq.reshape(-1, 3), (mesh.n_cells * 8, vec)).reshape(-1, 8, vec)
     fe = np.einsum("nqv,qi,nq->niv", b, shape_values_at_gauss(), cell_jxw(mesh))
     edofs = mesh.cells[:, :, None] * vec + np.arange(vec)
-    np.add.at(f, edofs.ravel(), fe.ravel())
-    return f
+    return f + _ordered_scatter(edofs.ravel(), fe.ravel(), f.size)
 
 
 def check_supported(problem):

@@ -391,9 +391,9 @@ int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *dat
     m->nbr_ptr = c->nbr_ptr;
     m->nbr = c->nbr;
     m->indptr = c->indptr;
-    // Bulk-copy pipelined SpMV is opt-in: measured 4.58 TB/s vs 5.36 TB/s for the register-
-    // streaming kernel on config 3 (profiles/r01_spmv_variants.md).
-    if (getenv("B200FEM_SPMV_TMA")) {
+    // Bulk-copy pipelined SpMV (default): 6.30 TB/s vs 5.36 TB/s for the register-streaming
+    // kernel on config 3 (profiles/r01_spmv_variants.md); B200FEM_SPMV_LDG=1 selects the latter.
+    if (!getenv("B200FEM_SPMV_LDG")) {
       int st = prepare_fem3_chunks(m);
       if (st) {
         delete m;

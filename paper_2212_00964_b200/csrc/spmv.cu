@@ -161,19 +161,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__rest
 }
 
 // ------------------------------------------------------------------------------------
-// FEM3 SpMV, Blackwell bulk-copy pipeline.  One persistent CTA per SM: a producer lane
-// streams contiguous node chunks (their CSR values and neighbour lists, which are
-// contiguous in memory for consecutive nodes) into a 4-stage shared-memory ring with
-// cp.async.bulk + mbarrier complete_tx; 16 consumer warps compute the node rows from
-// shared memory and gather x from L2.  The copy engine keeps ~150 KB per SM in flight
-// without spending registers, which is what the register-limited LDG kernel above
-// cannot do.  Same arithmetic and summation order as k_spmv_fem3 -> bit-identical y.
-constexpr int kTmaConsumers = 16;
+// FEM3 SpMV, Blackwell bulk-copy pipeline.  One persistent 1024-thread CTA per SM: a
+// producer lane streams contiguous node chunks (their CSR values and neighbour lists are
+// contiguous in memory for consecutive nodes) into a 3-stage shared-memory ring with
+// cp.async.bulk + mbarrier complete_tx; 31 consumer warps take one node each per chunk,
+// gather x from L2 and read the values from shared memory.  The copy engine keeps up to
+// two 60 KB chunks per SM in flight without spending registers.  Same per-lane arithmetic
+// and reduction tree as k_spmv_fem3 -> bit-identical y.
+constexpr int kTmaConsumers = 31;
 constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
-constexpr int kTmaStages = 4;
-constexpr int kTmaValBytes = 44 * 1024;
-constexpr int kTmaNbrBytes = 2560;
-constexpr int kTmaStageBytes = kTmaValBytes + kTmaNbrBytes;
+constexpr int kTmaStages = 3;
+constexpr int kTmaValBytes = 62 * 1024;
+constexpr int kTmaNbrBytes = 4096;
+constexpr int kTmaExtBytes = 768;  // one row-operand array of a chunk (<= 93 rows + alignment slack)
+constexpr int kTmaStageBytes = kTmaValBytes + kTmaNbrBytes + 3 * kTmaExtBytes;
 constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -205,6 +206,32 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                : "memory");
 }
 
+// Row operands of the epilogue, streamed into the stage with the values (so the row lanes
+// read them from shared memory instead of issuing scattered 8-byte loads).
+template <int MODE>
+__host__ __device__ constexpr int n_ext() {
+  return MODE == SP_JACOBI_R0 ? 2 : MODE == SP_JACOBI_TT ? 2 : MODE == SP_RESIDUAL ? 3 : MODE == SP_PQ ? 1
+       : MODE == SP_CGRES ? 2 : 0;
+}
+template <int MODE>
+__device__ __forceinline__ const double *ext_ptr(const SpmvArgs &a, int k) {
+  if (MODE == SP_JACOBI_R0) return k == 0 ? a.inv : a.aux;
+  if (MODE == SP_JACOBI_TT) return k == 0 ? a.inv : a.x;
+  if (MODE == SP_RESIDUAL) return k == 0 ? a.inv : (k == 1 ? a.aux : a.dg);
+  if (MODE == SP_PQ) return a.x;
+  return k == 0 ? a.inv : a.aux;  // SP_CGRES
+}
+template <int MODE>
+__device__ __forceinline__ RowPre row_pre_from(const double *e0, const double *e1, const double *e2) {
+  RowPre p{0.0, 0.0, 0.0, 0.0};
+  if (MODE == SP_JACOBI_R0) p.inv = *e0, p.aux = *e1;
+  else if (MODE == SP_JACOBI_TT) p.inv = *e0, p.xi = *e1;
+  else if (MODE == SP_RESIDUAL) p.inv = *e0, p.aux = *e1, p.dg = *e2;
+  else if (MODE == SP_PQ) p.xi = *e0;
+  else if (MODE == SP_CGRES) p.inv = *e0, p.aux = *e1;
+  return p;
+}
+
 // One node's three row sums from a value block `sv` (stage or global) and its neighbour ids.
 __device__ __forceinline__ void node_rows(const double *sv, const int32_t *sn, int cnt, const double *__restrict__ x,
                                           int lane, double &y0, double &y1, double &y2) {
@@ -225,7 +252,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
                                                                  const int32_t *__restrict__ nbr,
                                                                  const double *__restrict__ data,
                                                                  const int32_t *__restrict__ chunk_node, int n_chunks,
-                                                                 int64_t total_blocks, SpmvArgs a, RedScratch red) {
+                                                                 int64_t total_blocks, int64_t n_rows, SpmvArgs a,
+                                                                 RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kTmaStageBytes);
@@ -241,6 +269,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
   __syncthreads();
   // the last chunk's end may not be 16-byte aligned: it is read from global memory instead
   const uint64_t val_end = (uint64_t)total_blocks * 72, nbr_end = (uint64_t)total_blocks * 4;
+  const uint64_t row_end = (uint64_t)n_rows * 8;
   double red0 = 0.0, red1 = 0.0;
   if (warp == kTmaConsumers) {
     if (lane == 0) {  // producer
@@ -252,11 +281,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
         const int64_t p0 = __ldg(nbr_ptr + __ldg(chunk_node + c)), p1 = __ldg(nbr_ptr + __ldg(chunk_node + c + 1));
         const uint64_t vb0 = (72ull * p0) & ~15ull, vb1 = std::min((72ull * p1 + 15) & ~15ull, val_end & ~15ull);
         const uint64_t nb0 = (4ull * p0) & ~15ull, nb1 = std::min((4ull * p1 + 15) & ~15ull, nbr_end & ~15ull);
-        mbar_expect_tx(full + s, (uint32_t)((vb1 - vb0) + (nb1 - nb0)));
+        const int64_t cn0 = __ldg(chunk_node + c), cn1 = __ldg(chunk_node + c + 1);
+        const uint64_t eb0 = (24ull * cn0) & ~15ull, eb1 = std::min((24ull * cn1 + 15) & ~15ull, row_end & ~15ull);
+        const uint32_t ext_bytes = eb1 > eb0 ? (uint32_t)(eb1 - eb0) : 0u;
+        mbar_expect_tx(full + s, (uint32_t)((vb1 - vb0) + (nb1 - nb0)) + n_ext<MODE>() * ext_bytes);
         uint8_t *stage = smem + s * kTmaStageBytes;
         if (vb1 > vb0) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(data) + vb0, (uint32_t)(vb1 - vb0), full + s);
         if (nb1 > nb0)
           bulk_g2s(stage + kTmaValBytes, reinterpret_cast<const uint8_t *>(nbr) + nb0, (uint32_t)(nb1 - nb0), full + s);
+#pragma unroll
+        for (int k = 0; k < n_ext<MODE>(); ++k)
+          if (ext_bytes)
+            bulk_g2s(stage + kTmaValBytes + kTmaNbrBytes + k * kTmaExtBytes,
+                     reinterpret_cast<const uint8_t *>(ext_ptr<MODE>(a, k)) + eb0, ext_bytes, full + s);
       }
     }
     __syncwarp();  // reconverge the producer warp before the block-wide reduction barrier
@@ -268,48 +305,43 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
       const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
       const int64_t pc = __ldg(nbr_ptr + n0), pe = __ldg(nbr_ptr + n1);
       const uint64_t vb0 = (72ull * pc) & ~15ull, nb0 = (4ull * pc) & ~15ull;
-      const bool tail = (72ull * pe > (val_end & ~15ull)) || (4ull * pe > (nbr_end & ~15ull));
+      const bool tail = (72ull * pe > (val_end & ~15ull)) || (4ull * pe > (nbr_end & ~15ull)) ||
+                        (n_ext<MODE>() > 0 && 24ull * n1 > (row_end & ~15ull));
+      const uint64_t eb0 = (24ull * n0) & ~15ull;
       const uint8_t *stage = smem + s * kTmaStageBytes;
-      // prefetch this warp's node bounds and epilogue operands while the stage lands
-      int nA = n0 + warp, nB = n0 + warp + kTmaConsumers;
-      int64_t pA = 0, pB = 0;
-      int cA = 0, cB = 0;
-      if (nA < n1) {
+      const int nA = n0 + warp;
+      const bool has = nA < n1;
+      int64_t pA = 0;
+      int cA = 0;
+      if (has) {
         pA = __ldg(nbr_ptr + nA);
         cA = __ldg(nbr_ptr + nA + 1) - (int)pA;
       }
-      if (nB < n1) {
-        pB = __ldg(nbr_ptr + nB);
-        cB = __ldg(nbr_ptr + nB + 1) - (int)pB;
-      }
       const bool row_lane = (lane & 7) == 0 && lane < 24;
-      RowPre preA{0.0, 0.0, 0.0, 0.0}, preB{0.0, 0.0, 0.0, 0.0};
-      if (row_lane && nA < n1) preA = spmv_preload<MODE>(3 * (int64_t)nA + (lane >> 3), a);
-      if (row_lane && nB < n1) preB = spmv_preload<MODE>(3 * (int64_t)nB + (lane >> 3), a);
+      const int64_t row = 3 * (int64_t)nA + (lane >> 3);
+      RowPre pre{0.0, 0.0, 0.0, 0.0};
+      if (tail && row_lane && has) pre = spmv_preload<MODE>(row, a);
       mbar_wait(full + s, ph);
-      double yA0 = 0.0, yA1 = 0.0, yA2 = 0.0, yB0 = 0.0, yB1 = 0.0, yB2 = 0.0;
-      if (!tail) {
-        if (nA < n1)
+      if (!tail && row_lane && has && n_ext<MODE>() > 0) {
+        const uint8_t *ext = stage + kTmaValBytes + kTmaNbrBytes + (8ull * row - eb0);
+        pre = row_pre_from<MODE>(reinterpret_cast<const double *>(ext),
+                                 reinterpret_cast<const double *>(ext + kTmaExtBytes),
+                                 reinterpret_cast<const double *>(ext + 2 * kTmaExtBytes));
+      }
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      if (has) {
+        if (!tail)
           node_rows(reinterpret_cast<const double *>(stage + (72ull * pA - vb0)),
-                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0)), cA, a.x, lane, yA0,
-                    yA1, yA2);
-        if (nB < n1)
-          node_rows(reinterpret_cast<const double *>(stage + (72ull * pB - vb0)),
-                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pB - nb0)), cB, a.x, lane, yB0,
-                    yB1, yB2);
-      } else {
-        if (nA < n1) node_rows(data + 9 * pA, nbr + pA, cA, a.x, lane, yA0, yA1, yA2);
-        if (nB < n1) node_rows(data + 9 * pB, nbr + pB, cB, a.x, lane, yB0, yB1, yB2);
+                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0)), cA, a.x, lane, y0, y1,
+                    y2);
+        else
+          node_rows(data + 9 * pA, nbr + pA, cA, a.x, lane, y0, y1, y2);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);  // stage reads done; the producer may refill it
-      if (nA < n1) {
-        const double acc = warp_sum3(yA0, yA1, yA2, lane);
-        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nA + (lane >> 3), acc, a, preA, red0, red1);
-      }
-      if (nB < n1) {
-        const double acc = warp_sum3(yB0, yB1, yB2, lane);
-        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nB + (lane >> 3), acc, a, preB, red0, red1);
+      if (has) {
+        const double acc = warp_sum3(y0, y1, y2, lane);
+        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nA + (lane >> 3), acc, a, pre, red0, red1);
       }
     }
   }
@@ -321,7 +353,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
 }
 
 // Pack consecutive nodes into chunks whose values + neighbour ids fit one stage
-// (with 16-byte alignment slack).  Requires every chunk to hold <= 2*kTmaConsumers nodes.
+// (with 16-byte alignment slack), at most one node per consumer warp.
 int prepare_fem3_chunks(Matrix *m) {
   const int64_t nn = m->n / 3;
   std::vector<int32_t> ptr(nn + 1);
@@ -331,7 +363,7 @@ int prepare_fem3_chunks(Matrix *m) {
   int64_t start = 0;
   for (int64_t n = 0; n < nn; ++n) {
     const int64_t nb = ptr[n + 1] - ptr[start];
-    const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= 2 * kTmaConsumers;
+    const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= kTmaConsumers;
     if (!fits) {
       if (n == start) return 0;  // a single node does not fit a stage: keep the LDG kernel
       ch.push_back((int32_t)n);
@@ -410,7 +442,7 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = std::min(sms, m->n_chunks);
     k_spmv_fem3_tma<MODE><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
-                                                                  m->n_chunks, m->nnz / 9, a, r);
+                                                                  m->n_chunks, m->nnz / 9, m->n, a, r);
   } else if (m->kind == MK_FEM3) {
     const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n / 3 : m->row_hi;
     k_spmv_fem3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->data, lo, hi, a, r);

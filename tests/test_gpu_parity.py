@@ -334,16 +334,15 @@ def test_device_tensors_stay_on_device():
     assert isinstance(Us, torch.Tensor) and Us.is_cuda and rep.converged
 
 
-@pytest.mark.skip(reason="opt-in bulk-copy SpMV (B200FEM_SPMV_TMA) is experimental; see profiles/")
 def test_bulk_copy_spmv_bit_identical_to_ldg_kernel(rng, monkeypatch):
     """The cp.async.bulk pipelined FEM3 SpMV and the register-streaming kernel agree bitwise."""
     _, prob, U = build("nh_block", dict(CASES["nh_block"], dims=(9, 7, 5)))
     K = fem.assemble_jacobian(prob, U)
     x = rng.standard_normal(prob.n_dofs)
-    y_ldg = K @ x
-    monkeypatch.setenv("B200FEM_SPMV_TMA", "1")
+    y_tma = K @ x
+    monkeypatch.setenv("B200FEM_SPMV_LDG", "1")
     K2 = fem.assemble_jacobian(prob, U)
-    y_tma = K2 @ x
+    y_ldg = K2 @ x
     assert np.array_equal(y_tma, y_ldg)
     b = rng.standard_normal(prob.n_dofs)
     cfg = fem.LinearSolveConfig(rel_tol=1e-12, abs_tol=1e-14)

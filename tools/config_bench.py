@@ -1,0 +1,126 @@
+"""Throughput of the other BASELINE configs on one B200 (device-timed, CUDA events).
+
+    python tools/config_bench.py [--only c1,c2,c4,c5] [--c4n 40]
+
+c1: LE cantilever 20x4x4, incremental_solve(ramp(1))              (CPU-reference config)
+c2: Poisson 100^3 (1.03M DOF), source 1, zero on all faces        one Newton step, BiCGSTAB and PCG
+c4: J2 n^3, z=0 clamped, u_z = 0.012 ramp_and_back(10)            20 load steps with history commit
+c5: SIMP-LE 176x88x22, theta ~ U(0.3, 0.9) seeds 0..9             one Newton solve per design (warm start)
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2212_00964_b200 as fem  # noqa: E402
+from paper_2212_00964_b200 import _device as D  # noqa: E402
+
+ALU = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0
+
+
+def c1():
+    mesh = fem.generate_box_mesh(20, 4, 4, 20.0, 4.0, 4.0)
+    x0 = fem.BoundaryLocator.plane(0, 0.0)
+    specs = [fem.DirichletSpec(x0, c, lambda p: 0.0) for c in range(3)]
+    neu = [fem.NeumannSpec(fem.boundary_facets(mesh, fem.BoundaryLocator.plane(0, 20.0)),
+                           lambda p: np.broadcast_to([0.0, 0.0, -1.0], np.asarray(p).shape[:-1] + (3,)))]
+    prob = fem.LinearElasticityProblem(mesh, ALU, specs, neu)
+    fem.incremental_solve(prob, fem.LoadSchedule.ramp(1), reaction_locator=x0)  # warm-up incl. setup
+    prob2 = fem.LinearElasticityProblem(mesh, ALU, specs, neu)
+    h, dev, wall = timed(lambda: fem.incremental_solve(prob2, fem.LoadSchedule.ramp(1), reaction_locator=x0))
+    r = h.steps[0]
+    return {"config": "c1 LE cantilever 20x4x4", "n_dofs": prob.n_dofs, "wall_s_incl_setup": wall,
+            "device_s": dev, "newton_its": r.newton_iterations, "reaction_z": r.reaction,
+            "norm_U": float(np.linalg.norm(r.U)), "reference_cpu_s": "2.31 (SURVEY Appendix B, reference package)"}
+
+
+def c2():
+    n = 100
+    mesh = fem.generate_box_mesh(n, n, n, 1.0, 1.0, 1.0)
+    onb = fem.BoundaryLocator(lambda p: (np.abs(np.asarray(p) - 0.5) >= 0.5 - 1e-9).any(axis=-1))
+    out = {"config": "c2 Poisson 100^3", "n_cells": mesh.n_cells}
+    for method in ("bicgstab", "pcg"):
+        prob = fem.PoissonProblem(mesh, 1.0, [fem.DirichletSpec(onb, 0, lambda p: 0.0)],
+                                  source=lambda p: np.ones(np.asarray(p).shape[:-1] + (1,)))
+        _, setup, _ = timed(lambda: fem.workspace(prob))
+        lin = fem.LinearSolveConfig(method=method)
+        fem.newton_solve(prob, D.zeros(prob.n_dofs), lin_cfg=lin)  # warm-up (K cached: jacobian_constant)
+        prob._jac_cache = None
+        (U, rep), dev, _ = timed(lambda: fem.newton_solve(prob, D.zeros(prob.n_dofs), lin_cfg=lin))
+        out[method] = {"newton_s": dev, "setup_s": setup, "linear_iterations": [s.iterations for s in rep.linear_stats],
+                       "matvecs": sum(s.matvecs for s in rep.linear_stats), "max_u": float(U.max()),
+                       "norms": rep.residual_norms}
+    out["n_dofs"] = prob.n_dofs
+    out["reference_max_u"] = "5.622140e-02 (SURVEY 8(d), reference BiCGSTAB, 200 matvecs)"
+    return out
+
+
+def c4(n):
+    mesh = fem.generate_box_mesh(n, n, n, 1.0, 1.0, 1.0)
+    bot, top = fem.BoundaryLocator.plane(2, 0.0), fem.BoundaryLocator.plane(2, 1.0)
+    specs = [fem.DirichletSpec(bot, c, lambda p: 0.0) for c in range(3)] + [
+        fem.DirichletSpec(top, 2, lambda p: 0.012)]
+    prob = fem.J2PlasticityProblem(mesh, ALU, specs)
+    fem.workspace(prob)
+    sched = fem.LoadSchedule.ramp_and_back(10)
+    h, dev, wall = timed(lambda: fem.incremental_solve(prob, sched, reaction_locator=top))
+    return {"config": f"c4 J2 {n}^3 ramp_and_back(10)", "n_dofs": prob.n_dofs, "device_s": dev, "wall_s": wall,
+            "newton_its": [r.newton_iterations for r in h.steps], "reactions": [r.reaction for r in h.steps]}
+
+
+def c5(method="bicgstab"):
+    mesh = fem.generate_box_mesh(176, 88, 22, 8.0, 4.0, 1.0)
+    x0 = fem.BoundaryLocator.plane(0, 0.0)
+    specs = [fem.DirichletSpec(x0, c, lambda p: 0.0) for c in range(3)]
+    neu = [fem.NeumannSpec(fem.boundary_facets(mesh, fem.BoundaryLocator.plane(0, 8.0)),
+                           lambda p: np.broadcast_to([0.0, 0.0, -1.0], np.asarray(p).shape[:-1] + (3,)))]
+    prob = fem.SimpElasticityProblem(mesh, fem.LinearElastic(ALU), specs, neu, penalty=3.0)
+    fem.workspace(prob)
+    lin = fem.LinearSolveConfig(method=method)
+    U = D.zeros(prob.n_dofs)
+    times, its = [], []
+    for k in range(10):
+        prob.set_theta(np.random.default_rng(k).uniform(0.3, 0.9, mesh.n_cells))
+        (U, rep), dev, _ = timed(lambda: fem.newton_solve(prob, U, lin_cfg=lin))
+        times.append(dev)
+        its.append([s.iterations for s in rep.linear_stats])
+    return {"config": f"c5 SIMP-LE 176x88x22 ({method})", "n_dofs": prob.n_dofs, "per_design_s": times,
+            "mean_design_s": float(np.mean(times[1:])), "linear_iterations": its}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c1,c2,c4,c5")
+    ap.add_argument("--c4n", type=int, default=40)
+    a = ap.parse_args()
+    res = []
+    for name in a.only.split(","):
+        if name == "c1":
+            res.append(c1())
+        elif name == "c2":
+            res.append(c2())
+        elif name == "c4":
+            res.append(c4(a.c4n))
+        elif name == "c5":
+            res.append(c5("bicgstab"))
+            res.append(c5("pcg"))
+        print(json.dumps(res[-1]), flush=True)
