@@ -128,6 +128,13 @@ int b200fem_commit_state(b200fem_ctx *ctx, const double *U_dev);
 /* ---- sparse operators (sparse.py:15-51, kernels.py:37-47) ---- */
 /* FEM matrix on this ctx's pattern (uses the node-blocked index, no indices array) */
 int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *data_dev);
+/* Symmetric node-block operator (vec 3): the upper 3x3 node blocks of the tangent before
+ * the Dirichlet row replacement (b200fem_jacobian_sym), applied with identity Dirichlet rows.
+ * Same operator as the CSR Jacobian of this ctx with half of the value traffic. */
+int b200fem_ctx_sym_size(const b200fem_ctx *ctx, int64_t *n_values);
+int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U_dev, double *data_dev /* nullable */,
+                         double *sym_dev, b200fem_error *err);
+int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double *sym_dev);
 /* generic CSR on the device (any square matrix with sorted unique columns) */
 int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr_dev,
                        const int32_t *indices_dev, const double *data_dev, void *stream);

@@ -78,6 +78,9 @@ SIGNATURES = {
     "b200fem_commit_state": (C.c_int, [_vp, _vp]),
     "b200fem_matrix_fem": (C.c_int, [C.POINTER(_vp), _vp, _vp]),
     "b200fem_matrix_csr": (C.c_int, [C.POINTER(_vp), _i64, _i64, _vp, _vp, _vp, _vp]),
+    "b200fem_ctx_sym_size": (C.c_int, [_vp, _pi64]),
+    "b200fem_jacobian_sym": (C.c_int, [_vp, _vp, _vp, _vp, _perr]),
+    "b200fem_matrix_fem_sym": (C.c_int, [C.POINTER(_vp), _vp, _vp]),
     "b200fem_matrix_set_data": (C.c_int, [_vp, _vp]),
     "b200fem_matrix_destroy": (C.c_int, [_vp]),
     "b200fem_matvec": (C.c_int, [_vp, _vp, _vp]),

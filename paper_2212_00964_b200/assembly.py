@@ -239,6 +239,23 @@ class DeviceWorkspace:
         st = _lib.lib().b200fem_jacobian(self.ctx, D.ptr(U), D.ptr(data), C.byref(err))
         raise_for(st, err, "jacobian")
 
+    @property
+    def has_sym(self) -> bool:
+        return self.vec == 3
+
+    def sym_size(self) -> int:
+        n = C.c_int64()
+        raise_for(_lib.lib().b200fem_ctx_sym_size(self.ctx, C.byref(n)), None, "sym_size")
+        return n.value
+
+    def jacobian_sym(self, problem, U, sym, data=None):
+        """Upper symmetric node blocks of the tangent (and optionally the full CSR values)."""
+        self.sync(problem)
+        err = _lib.Error()
+        st = _lib.lib().b200fem_jacobian_sym(self.ctx, D.ptr(U), D.ptr(data) if data is not None else None,
+                                             D.ptr(sym), C.byref(err))
+        raise_for(st, err, "jacobian_sym")
+
     def qp_flux(self, problem, U):
         self.sync(problem)
         out = D.empty(self.n_cells * 8 * self.vec * 3)

@@ -185,6 +185,32 @@ __global__ void k_diag_slots(const int32_t *__restrict__ nbr_ptr, const int32_t 
   }
 }
 
+// symmetric storage maps: upper-block counts per node, then the block index of every
+// lower coupling (m < n) inside m's upper list
+__global__ void k_sym_count(const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr, int64_t n_nodes,
+                            int32_t *ucnt) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    const int p0 = nbr_ptr[n], cnt = nbr_ptr[n + 1] - p0;
+    ucnt[n] = cnt - find_sorted(nbr + p0, cnt, (int)n);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ucnt[n_nodes] = 0;
+}
+
+__global__ void k_sym_lower(const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr,
+                            const int32_t *__restrict__ up_ptr, int64_t n_nodes, int32_t *lo_blk) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    const int p0 = nbr_ptr[n], cnt = nbr_ptr[n + 1] - p0;
+    for (int j = 0; j < cnt; ++j) {
+      const int m = nbr[p0 + j];
+      if (m >= n) break;
+      const int q0 = nbr_ptr[m], qc = nbr_ptr[m + 1] - q0;
+      const int self_m = qc - (up_ptr[m + 1] - up_ptr[m]);
+      const int pos = find_sorted(nbr + q0, qc, (int)n);
+      lo_blk[p0 + j] = up_ptr[m] + (pos - self_m);
+    }
+  }
+}
+
 __global__ void k_indices(const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr,
                           const int32_t *__restrict__ indptr, int64_t n_nodes, int vec, int32_t *indices) {
   const int lane = threadIdx.x & 31;
@@ -245,7 +271,7 @@ static void free_ctx(Ctx *c) {
   if (!c) return;
   void *ptrs[] = {c->coords, c->cells, c->nbr_ptr, c->nbr, c->indptr, c->cpos, c->diag, c->color_cells,
                   c->dir_dofs, c->dir_vals, c->f_neumann, c->f_body, c->theta, c->eps_prev, c->sig_prev, c->derr,
-                  c->n2c_ptr, c->n2c, c->n2c_a, c->dir_flag, c->scratch};
+                  c->n2c_ptr, c->n2c, c->n2c_a, c->dir_flag, c->scratch, c->up_ptr, c->lo_blk};
   for (void *p : ptrs) cudaFree(p);
   if (c->indices && c->indices != c->nbr) cudaFree(c->indices);
   red_free(&c->red);
@@ -390,6 +416,21 @@ static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem
   k_diag_slots<<<grid_for(nn), kThreads, 0, s>>>(c->nbr_ptr, c->nbr, c->indptr, nn, c->vec, c->diag);
   count_launch();
   if (c->vec == 1) c->indices = c->nbr;  // vec 1: the node list IS the column list
+  if (c->vec == 3) {  // symmetric node-block storage maps
+    int32_t *ucnt = nullptr;
+    B200_CUDA_E(dalloc(&ucnt, nn + 1), err);
+    B200_CUDA_E(dalloc(&c->up_ptr, nn + 1), err);
+    k_sym_count<<<grid_for(nn), kThreads, 0, s>>>(c->nbr_ptr, c->nbr, nn, ucnt);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, ucnt, c->up_ptr, (int)(nn + 1), s);
+    B200_CUDA_E(dalloc(&c->lo_blk, total), err);
+    k_sym_lower<<<grid_for(nn), kThreads, 0, s>>>(c->nbr_ptr, c->nbr, c->up_ptr, nn, c->lo_blk);
+    count_launch(3);
+    int32_t nb = 0;
+    B200_CUDA_E(cudaMemcpyAsync(&nb, c->up_ptr + nn, sizeof(int32_t), cudaMemcpyDeviceToHost, s), err);
+    B200_CUDA_E(cudaStreamSynchronize(s), err);
+    cudaFree(ucnt);
+    c->n_sym_blocks = nb;
+  }
 
   // ---- colouring
   std::vector<int32_t> order;

@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
     const int32_t *__restrict__ n2c_ptr, const int32_t *__restrict__ n2c, const uint8_t *__restrict__ n2c_a,
     const uint8_t *__restrict__ cpos, const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr,
     const double *__restrict__ Ke, const uint8_t *__restrict__ dir_flag, int64_t n_nodes, int max_nbr,
-    double *__restrict__ data) {
+    double *__restrict__ data, const int32_t *__restrict__ up_ptr, double *__restrict__ sym) {
   extern __shared__ double gsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double *acc = gsm + (size_t)w * VEC * VEC * max_nbr;
@@ -668,12 +668,25 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
         if (pos[r] >= 0) acc[pos[r]] += v[r];
       __syncwarp();  // ascending cell order per slot
     }
-    if (dir_flag) {
-      int self = 0, hi = cnt;  // position of n in its own neighbour list
+    int self = 0;
+    if (dir_flag || sym) {
+      int hi = cnt;  // position of n in its own neighbour list
       while (self < hi) {
         const int mid = (self + hi) >> 1;
         if (__ldg(nbr + p0 + mid) < (int)n) self = mid + 1; else hi = mid;
       }
+    }
+    if (sym) {  // upper node blocks (m >= n), pre-Dirichlet, 3x3 row-major: the SYM3 operator
+      double *o = sym + (int64_t)VEC * VEC * __ldg(up_ptr + n);
+      const int nu = cnt - self;
+      for (int t = lane; t < nu * VEC * VEC; t += 32) {
+        const int jb = t / (VEC * VEC), rr = t - jb * VEC * VEC, i = rr / VEC, kk = rr - i * VEC;
+        o[t] = acc[i * L + VEC * (self + jb) + kk];
+      }
+      __syncwarp();
+    }
+    if (!data) continue;
+    if (dir_flag) {
       for (int i = 0; i < VEC; ++i) {
         if (!__ldg(dir_flag + n * VEC + i)) continue;
         for (int t = lane; t < L; t += 32) acc[i * L + t] = (t == VEC * self + i) ? 1.0 : 0.0;
@@ -928,7 +941,7 @@ int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int app
 
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
-int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err) {
+int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym) {
   cudaStream_t s = c->stream;
   const int vv = c->vec * c->vec;
   if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
@@ -948,12 +961,12 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_jacobian_gather<3><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
                                                      c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
-                                                     c->max_nbr, data);
+                                                     c->max_nbr, data, c->up_ptr, sym);
   } else {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_jacobian_gather<1><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
                                                      c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
-                                                     c->max_nbr, data);
+                                                     c->max_nbr, data, nullptr, nullptr);
   }
   count_launch(2);
   B200_CUDA_E(cudaGetLastError(), err);
@@ -1010,7 +1023,14 @@ int b200fem_residual(b200fem_ctx *ctx, const double *U, double bc_scale, int32_t
 
 int b200fem_jacobian(b200fem_ctx *ctx, const double *U, double *data, b200fem_error *err) {
   if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
-  return launch_jacobian((Ctx *)ctx, U, data, err);
+  return launch_jacobian((Ctx *)ctx, U, data, err, nullptr);
+}
+
+int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U, double *data, double *sym, b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  Ctx *c = (Ctx *)ctx;
+  if (c->vec != 3 || !sym) return B200FEM_E_INVALID;
+  return launch_jacobian(c, U, data, err, sym);
 }
 
 int b200fem_qp_flux(b200fem_ctx *ctx, const double *U, double *out, b200fem_error *err) {

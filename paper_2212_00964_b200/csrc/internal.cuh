@@ -92,6 +92,11 @@ struct Ctx {
   int32_t *indices = nullptr; // lazily materialised (vec==1 aliases nbr)
   uint8_t *cpos = nullptr;    // (n_cells,64) position of node b in node a's neighbour list
   int32_t *diag = nullptr;    // (n_dofs) diagonal slot
+  // symmetric node-block storage (vec 3): upper blocks (m >= n) of node n at up_ptr[n],
+  // 3x3 row-major; lo_blk[nbr_ptr[n] + j] = block index of (m, n) for the lower neighbours
+  int32_t *up_ptr = nullptr;  // (n_nodes+1)
+  int32_t *lo_blk = nullptr;  // (total neighbours) only lower entries used
+  int64_t n_sym_blocks = 0;
   int max_nbr = 0;
   int max_deg = 0;              // max cells per node
   int32_t *n2c_ptr = nullptr;   // (n_nodes+1) node -> incident cells, ascending cell id
@@ -128,7 +133,7 @@ struct KrylovWork {
   cudaEvent_t ev[2]{};
 };
 
-enum MatKind : int { MK_CSR = 0, MK_FEM3 = 1 };
+enum MatKind : int { MK_CSR = 0, MK_FEM3 = 1, MK_SYM3 = 2 };
 struct Matrix {
   MatKind kind = MK_CSR;
   int64_t n = 0, nnz = 0;
@@ -149,6 +154,9 @@ struct Matrix {
   // space stays in {v : v_d = 0}, where the row-replaced K acts as the SPD block K_ff
   const int32_t *dir_dofs = nullptr;
   int64_t n_dir = 0;
+  // SYM3: upper node blocks (pre-Dirichlet) + Dirichlet row flags applied on output rows
+  const int32_t *up_ptr = nullptr, *lo_blk = nullptr;
+  const uint8_t *dir_flag = nullptr;
 };
 
 // allocation helpers
@@ -182,11 +190,12 @@ struct SpmvArgs {
 int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
 int prepare_fem3_chunks(Matrix *m);
+int prepare_sym3_chunks(Matrix *m);
 
 // element kernels
 int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int apply_dirichlet,
                     b200fem_error *err, double *norm_host);
-int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err);
+int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym = nullptr);
 int launch_qp_flux(Ctx *c, const double *U, double *out, b200fem_error *err);
 int launch_volume_average(Ctx *c, const double *U, double *out_host, b200fem_error *err);
 int launch_commit(Ctx *c, const double *U);

@@ -410,6 +410,41 @@ int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *dat
   return 0;
 }
 
+int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double *sym) {
+  Ctx *c = (Ctx *)ctx;
+  if (!out || !c || c->vec != 3) return B200FEM_E_INVALID;
+  Matrix *m = new Matrix();
+  m->kind = MK_SYM3;
+  m->n = c->n_dofs;
+  m->nnz = c->nnz;
+  m->data = sym;
+  m->stream = c->stream;
+  m->nbr_ptr = c->nbr_ptr;
+  m->nbr = c->nbr;
+  m->indptr = c->indptr;
+  m->up_ptr = c->up_ptr;
+  m->lo_blk = c->lo_blk;
+  m->dir_flag = c->n_dir ? c->dir_flag : nullptr;
+  m->dir_dofs = c->dir_dofs;
+  m->n_dir = c->n_dir;
+  if (getenv("B200FEM_SYM_TMA")) {  // bulk-copy variant: 2.83 ms vs 1.64 ms LDG (L2-gather bound)
+    int st = prepare_sym3_chunks(m);
+    if (st) {
+      delete m;
+      return st;
+    }
+  }
+  *out = (b200fem_matrix *)m;
+  return 0;
+}
+
+int b200fem_ctx_sym_size(const b200fem_ctx *ctx, int64_t *n_values) {
+  const Ctx *c = (const Ctx *)ctx;
+  if (!c || c->vec != 3) return B200FEM_E_INVALID;
+  *n_values = 9 * c->n_sym_blocks;
+  return 0;
+}
+
 int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr, const int32_t *indices,
                        const double *data, void *stream) {
   if (!out || n < 0 || nnz < 0) return B200FEM_E_INVALID;

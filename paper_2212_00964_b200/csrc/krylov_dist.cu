@@ -378,11 +378,11 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
   if (!out || !m || own_node_lo < 0 || own_node_hi < own_node_lo) return B200FEM_E_INVALID;
   Part *P = new Part();
   P->m = m;
-  P->vec = m->kind == MK_FEM3 ? 3 : 1;
+  P->vec = m->kind == MK_CSR ? 1 : 3;
   P->own_lo = own_node_lo;
   P->own_hi = own_node_hi;
-  m->row_lo = own_node_lo * (m->kind == MK_FEM3 ? 1 : P->vec);
-  m->row_hi = own_node_hi * (m->kind == MK_FEM3 ? 1 : P->vec);
+  m->row_lo = own_node_lo;  // node range (FEM3/SYM3) == row range (vec-1 CSR)
+  m->row_hi = own_node_hi;
   m->use_tma = false;
   P->n_peers = n_peers;
   P->peer.assign(peers, peers + n_peers);

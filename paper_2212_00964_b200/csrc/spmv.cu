@@ -161,6 +161,85 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__rest
 }
 
 // ------------------------------------------------------------------------------------
+// SYM3: symmetric node-block operator.  The assembled tangent of every supported law is
+// exactly symmetric before the Dirichlet row replacement (K_mn = K_nm^T bit for bit: each
+// per-cell block pair is one stored block and its transpose, summed in the same cell order),
+// so only the upper blocks (m >= n, 3x3 row-major) are stored: 14 of 27 blocks per interior
+// node.  Row n = sum over upper blocks B_nm x_m + sum over lower neighbours B_mn^T x_m; the
+// lower blocks were streamed moments earlier as upper blocks of rows m < n and are served
+// by L2.  Dirichlet rows act as identity rows (y_d = x_d), exactly the row-replaced K of
+// assembly.py:297-299.  DRAM bytes per matvec drop from 8 B/nnz to ~4.2 B/nnz.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) k_spmv_sym3(const int32_t *__restrict__ nbr_ptr,
+                                                           const int32_t *__restrict__ nbr,
+                                                           const int32_t *__restrict__ up_ptr,
+                                                           const int32_t *__restrict__ lo_blk,
+                                                           const double *__restrict__ sym,
+                                                           const uint8_t *__restrict__ dir_flag, int64_t node_lo,
+                                                           int64_t n_nodes, SpmvArgs a, RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double *__restrict__ x = a.x;
+  double red0 = 0.0, red1 = 0.0;
+  // metadata of the warp's next node is prefetched one node ahead so that the block and
+  // x loads of a node are issued in a single memory round trip
+  int64_t n = node_lo + warp0;
+  int nx_p0 = 0, nx_cnt = 0, nx_ub = 0, nx_uc = 0, nx_m = 0, nx_lb = 0;
+  auto fetch = [&](int64_t k) {
+    nx_p0 = __ldg(nbr_ptr + k);
+    nx_cnt = __ldg(nbr_ptr + k + 1) - nx_p0;
+    nx_ub = __ldg(up_ptr + k);
+    nx_uc = __ldg(up_ptr + k + 1) - nx_ub;
+    nx_m = lane < nx_cnt ? __ldg(nbr + nx_p0 + lane) : 0;
+    nx_lb = lane < nx_cnt - nx_uc ? __ldg(lo_blk + nx_p0 + lane) : 0;
+  };
+  if (n < n_nodes) fetch(n);
+  for (; n < n_nodes; n += nwarps) {
+    const int p0 = nx_p0, cnt = nx_cnt, ub = nx_ub, self = cnt - nx_uc, m0 = nx_m, lb0 = nx_lb;
+    const bool row_lane = (lane & 7) == 0 && lane < 24;
+    const int64_t row = 3 * n + (lane >> 3);
+    RowPre pre{0.0, 0.0, 0.0, 0.0};
+    bool dflag = false;
+    double xrow = 0.0;
+    if (row_lane) {
+      pre = spmv_preload<MODE>(row, a);
+      dflag = dir_flag && __ldg(dir_flag + row);
+      if (dflag) xrow = __ldg(x + row);
+    }
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    for (int j = lane; j < cnt; j += 32) {
+      const int m = j == lane ? m0 : __ldg(nbr + p0 + j);
+      const bool lower = j < self;
+      const int blk = lower ? (j == lane ? lb0 : __ldg(lo_blk + p0 + j)) : ub + (j - self);
+      const double *__restrict__ B = sym + 9 * (int64_t)blk;
+      const double b00 = __ldg(B), b01 = __ldg(B + 1), b02 = __ldg(B + 2);
+      const double b10 = __ldg(B + 3), b11 = __ldg(B + 4), b12 = __ldg(B + 5);
+      const double b20 = __ldg(B + 6), b21 = __ldg(B + 7), b22 = __ldg(B + 8);
+      const double *__restrict__ xm = x + 3 * (int64_t)m;
+      const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+      // lower neighbours use the transposed block
+      const double a01 = lower ? b10 : b01, a02 = lower ? b20 : b02, a10 = lower ? b01 : b10;
+      const double a12 = lower ? b21 : b12, a20 = lower ? b02 : b20, a21 = lower ? b12 : b21;
+      y0 = fma(a02, x2, fma(a01, x1, fma(b00, x0, y0)));
+      y1 = fma(a12, x2, fma(b11, x1, fma(a10, x0, y1)));
+      y2 = fma(b22, x2, fma(a21, x1, fma(a20, x0, y2)));
+    }
+    if (n + nwarps < n_nodes) fetch(n + nwarps);
+    double acc = warp_sum3(y0, y1, y2, lane);
+    if (row_lane) {
+      if (dflag) acc = xrow;  // identity row
+      spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+    }
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage) spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // FEM3 SpMV, Blackwell bulk-copy pipeline.  One persistent 1024-thread CTA per SM: a
 // producer lane streams contiguous node chunks (their CSR values and neighbour lists are
 // contiguous in memory for consecutive nodes) into a 3-stage shared-memory ring with
@@ -389,6 +468,182 @@ int prepare_fem3_chunks(Matrix *m) {
   return 0;
 }
 
+// ------------------------------------------------------------------------------------
+// SYM3 with the bulk-copy pipeline: the chunk's upper blocks, neighbour ids, lower-block
+// indices and row operands are contiguous for consecutive nodes and stream into shared
+// memory; the consumer warps gather only x and the lower blocks (L2-resident: they were
+// streamed as upper blocks of nearby rows moments before).  One memory round trip per node.
+constexpr int kSymUpBytes = 40 * 1024;
+constexpr int kSymNbrBytes = 4096;
+constexpr int kSymStageBytes = kSymUpBytes + 2 * kSymNbrBytes + 3 * kTmaExtBytes;
+constexpr int kSymStages = 4;
+constexpr int kSymSmem = kSymStages * kSymStageBytes + 2 * kSymStages * 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_sym3_tma(
+    const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr, const int32_t *__restrict__ up_ptr,
+    const int32_t *__restrict__ lo_blk, const double *__restrict__ sym, const uint8_t *__restrict__ dir_flag,
+    const int32_t *__restrict__ chunk_node, int n_chunks, int64_t n_nodes, SpmvArgs a, RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSymStages * kSymStageBytes);
+  uint64_t *empty = full + kSymStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSymStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t up_end = (uint64_t)__ldg(up_ptr + n_nodes) * 72, nb_end = (uint64_t)__ldg(nbr_ptr + n_nodes) * 4;
+  const uint64_t row_end = (uint64_t)n_nodes * 24;
+  double red0 = 0.0, red1 = 0.0;
+  if (warp == kTmaConsumers) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int s = it % kSymStages;
+        const uint32_t ph = (it / kSymStages) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        const int64_t n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
+        const uint64_t u0 = (72ull * __ldg(up_ptr + n0)) & ~15ull,
+                       u1 = std::min((72ull * __ldg(up_ptr + n1) + 15) & ~15ull, up_end & ~15ull);
+        const uint64_t b0 = (4ull * __ldg(nbr_ptr + n0)) & ~15ull,
+                       b1 = std::min((4ull * __ldg(nbr_ptr + n1) + 15) & ~15ull, nb_end & ~15ull);
+        const uint64_t e0 = (24ull * n0) & ~15ull, e1 = std::min((24ull * n1 + 15) & ~15ull, row_end & ~15ull);
+        const uint32_t ub = u1 > u0 ? (uint32_t)(u1 - u0) : 0u, nb = b1 > b0 ? (uint32_t)(b1 - b0) : 0u,
+                       eb = e1 > e0 ? (uint32_t)(e1 - e0) : 0u;
+        mbar_expect_tx(full + s, ub + 2 * nb + n_ext<MODE>() * eb);
+        uint8_t *stage = smem + s * kSymStageBytes;
+        if (ub) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(sym) + u0, ub, full + s);
+        if (nb) {
+          bulk_g2s(stage + kSymUpBytes, reinterpret_cast<const uint8_t *>(nbr) + b0, nb, full + s);
+          bulk_g2s(stage + kSymUpBytes + kSymNbrBytes, reinterpret_cast<const uint8_t *>(lo_blk) + b0, nb, full + s);
+        }
+#pragma unroll
+        for (int k = 0; k < n_ext<MODE>(); ++k)
+          if (eb)
+            bulk_g2s(stage + kSymUpBytes + 2 * kSymNbrBytes + k * kTmaExtBytes,
+                     reinterpret_cast<const uint8_t *>(ext_ptr<MODE>(a, k)) + e0, eb, full + s);
+      }
+    }
+    __syncwarp();
+  } else {
+    int it = 0;
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+      const int s = it % kSymStages;
+      const uint32_t ph = (it / kSymStages) & 1;
+      const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
+      const int64_t u0 = (72ll * __ldg(up_ptr + n0)) & ~15ll, b0 = (4ll * __ldg(nbr_ptr + n0)) & ~15ll;
+      const uint64_t e0 = (24ull * n0) & ~15ull;
+      const bool tail = (72ull * __ldg(up_ptr + n1) > (up_end & ~15ull)) ||
+                        (4ull * __ldg(nbr_ptr + n1) > (nb_end & ~15ull)) ||
+                        (n_ext<MODE>() > 0 && 24ull * n1 > (row_end & ~15ull));
+      const uint8_t *stage = smem + s * kSymStageBytes;
+      const int n = n0 + warp;
+      const bool has = n < n1;
+      int p0 = 0, cnt = 0, ubn = 0, self = 0;
+      if (has) {
+        p0 = __ldg(nbr_ptr + n);
+        cnt = __ldg(nbr_ptr + n + 1) - p0;
+        ubn = __ldg(up_ptr + n);
+        self = cnt - (__ldg(up_ptr + n + 1) - ubn);
+      }
+      const bool row_lane = (lane & 7) == 0 && lane < 24;
+      const int64_t row = 3 * (int64_t)n + (lane >> 3);
+      RowPre pre{0.0, 0.0, 0.0, 0.0};
+      bool dflag = false;
+      double xrow = 0.0;
+      if (row_lane && has) {
+        if (tail) pre = spmv_preload<MODE>(row, a);
+        dflag = dir_flag && __ldg(dir_flag + row);
+        if (dflag) xrow = __ldg(a.x + row);
+      }
+      mbar_wait(full + s, ph);
+      if (!tail && row_lane && has && n_ext<MODE>() > 0) {
+        const uint8_t *ext = stage + kSymUpBytes + 2 * kSymNbrBytes + (8ull * row - e0);
+        pre = row_pre_from<MODE>(reinterpret_cast<const double *>(ext),
+                                 reinterpret_cast<const double *>(ext + kTmaExtBytes),
+                                 reinterpret_cast<const double *>(ext + 2 * kTmaExtBytes));
+      }
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      if (has) {
+        const int32_t *sn = tail ? nbr + p0 : reinterpret_cast<const int32_t *>(stage + kSymUpBytes + (4ll * p0 - b0));
+        const int32_t *sl =
+            tail ? lo_blk + p0 : reinterpret_cast<const int32_t *>(stage + kSymUpBytes + kSymNbrBytes + (4ll * p0 - b0));
+        const double *su = tail ? sym + 9 * (int64_t)ubn : reinterpret_cast<const double *>(stage + (72ll * ubn - u0));
+        for (int j = lane; j < cnt; j += 32) {
+          const int m = sn[j];
+          const bool lower = j < self;
+          const double *B = lower ? sym + 9 * (int64_t)sl[j] : su + 9 * (j - self);
+          double bb[9];
+#pragma unroll
+          for (int t = 0; t < 9; ++t) bb[t] = lower ? __ldg(B + t) : B[t];
+          const double *__restrict__ xm = a.x + 3 * (int64_t)m;
+          const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+          const double a01 = lower ? bb[3] : bb[1], a02 = lower ? bb[6] : bb[2], a10 = lower ? bb[1] : bb[3];
+          const double a12 = lower ? bb[7] : bb[5], a20 = lower ? bb[2] : bb[6], a21 = lower ? bb[5] : bb[7];
+          y0 = fma(a02, x2, fma(a01, x1, fma(bb[0], x0, y0)));
+          y1 = fma(a12, x2, fma(bb[4], x1, fma(a10, x0, y1)));
+          y2 = fma(bb[8], x2, fma(a21, x1, fma(a20, x0, y2)));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      if (has) {
+        double acc = warp_sum3(y0, y1, y2, lane);
+        if (row_lane) {
+          if (dflag) acc = xrow;
+          spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+        }
+      }
+    }
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
+      spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
+int prepare_sym3_chunks(Matrix *m) {
+  const int64_t nn = m->n / 3;
+  std::vector<int32_t> ptr(nn + 1), up(nn + 1);
+  if (cudaMemcpy(ptr.data(), m->nbr_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(up.data(), m->up_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return B200FEM_E_CUDA;
+  std::vector<int32_t> ch{0};
+  int64_t start = 0;
+  for (int64_t n = 0; n < nn; ++n) {
+    const int64_t nu = up[n + 1] - up[start], nb = ptr[n + 1] - ptr[start];
+    const bool fits = 72 * nu + 32 <= kSymUpBytes && 4 * nb + 32 <= kSymNbrBytes && (n + 1 - start) <= kTmaConsumers;
+    if (!fits) {
+      if (n == start) return 0;
+      ch.push_back((int32_t)n);
+      start = n;
+    }
+  }
+  ch.push_back((int32_t)nn);
+  m->n_chunks = (int)ch.size() - 1;
+  if (dalloc(&m->chunk_node, ch.size()) != cudaSuccess) return B200FEM_E_CUDA;
+  if (cudaMemcpy(m->chunk_node, ch.data(), ch.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+    return B200FEM_E_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_CGRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    attr = true;
+  }
+  m->use_tma = true;
+  return 0;
+}
+
 template <int MODE, int LANES>
 __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict__ indptr,
                                                        const int32_t *__restrict__ indices,
@@ -443,6 +698,18 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     const int g = std::min(sms, m->n_chunks);
     k_spmv_fem3_tma<MODE><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
                                                                   m->n_chunks, m->nnz / 9, m->n, a, r);
+  } else if (m->kind == MK_SYM3 && m->use_tma && full) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = std::min(sms, m->n_chunks);
+    k_spmv_sym3_tma<MODE><<<g, kTmaThreads, kSymSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->up_ptr, m->lo_blk, m->data,
+                                                                  m->dir_flag, m->chunk_node, m->n_chunks, m->n / 3,
+                                                                  a, r);
+  } else if (m->kind == MK_SYM3) {
+    const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n / 3 : m->row_hi;
+    k_spmv_sym3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->up_ptr, m->lo_blk, m->data,
+                                                       m->dir_flag, lo, hi, a, r);
   } else if (m->kind == MK_FEM3) {
     const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n / 3 : m->row_hi;
     k_spmv_fem3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->data, lo, hi, a, r);
@@ -475,13 +742,17 @@ int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *r
 __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict__ indptr,
                                                        const int32_t *__restrict__ indices,
                                                        const int32_t *__restrict__ slots,
+                                                       const int32_t *__restrict__ up_ptr,
+                                                       const uint8_t *__restrict__ dflag,
                                                        const double *__restrict__ data, int64_t row_lo, int64_t n,
                                                        double *diag, double *inv, RedScratch red) {
   double zeros[1] = {0.0};
   for (int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double d = 0.0;
-    if (slots) {
+    if (up_ptr) {  // SYM3: entry (c,c) of the node's self block (first upper block)
+      d = (dflag && dflag[i]) ? 1.0 : data[9 * (int64_t)up_ptr[i / 3] + 4 * (i % 3)];
+    } else if (slots) {
       d = data[slots[i]];
     } else {
       int lo = indptr[i], hi = indptr[i + 1];
@@ -500,10 +771,13 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
 }
 
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero) {
-  const int64_t lo = m->row_hi < 0 ? 0 : (m->kind == MK_FEM3 ? 3 * m->row_lo : m->row_lo);
-  const int64_t hi = m->row_hi < 0 ? m->n : (m->kind == MK_FEM3 ? 3 * m->row_hi : m->row_hi);
-  k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, m->diag_slots, m->data, lo, hi, diag, inv,
-                                                     *red);
+  const bool nodes = m->kind != MK_CSR;
+  const int64_t lo = m->row_hi < 0 ? 0 : (nodes ? 3 * m->row_lo : m->row_lo);
+  const int64_t hi = m->row_hi < 0 ? m->n : (nodes ? 3 * m->row_hi : m->row_hi);
+  const bool sym = m->kind == MK_SYM3;
+  k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, sym ? nullptr : m->diag_slots,
+                                                     sym ? m->up_ptr : nullptr, sym ? m->dir_flag : nullptr, m->data,
+                                                     lo, hi, diag, inv, *red);
   count_launch();
   if (n_zero) {
     double z = 0.0;

@@ -20,7 +20,7 @@ from . import _lib
 from .assembly import workspace
 from .errors import BreakdownError, LinearSolverError, NonConvergenceError, raise_for
 from .mesh import BoundaryLocator, locate_nodes
-from .sparse import CsrMatrix
+from .sparse import CsrMatrix, SymOperator
 
 __all__ = ["LinearSolveConfig", "NewtonConfig", "LoadSchedule", "LinearSolverError", "BreakdownError",
            "NonConvergenceError", "bicgstab_jacobi", "pcg_jacobi", "newton_solve", "incremental_solve", "reaction_force",
@@ -35,12 +35,18 @@ class LinearSolveConfig:
     # "bicgstab" = the reference solver (solvers.py:87-167, default); "pcg" = Jacobi-CG for
     # symmetric tangents (north_star "CG/BiCGSTAB", BASELINE config 2), same stopping rule
     method: str = "bicgstab"
+    # operator of the Newton-loop solves: "csr" = the assembled CSR values (default);
+    # "sym" = symmetric node-block storage for vec-3 problems (same operator, half the DRAM
+    # bytes, but L2-gather bound: 1.64 ms vs 0.85 ms per config-3 matvec, profiles/)
+    operator: str = "csr"
 
     def __post_init__(self):
         if self.rel_tol <= 0 or self.abs_tol <= 0:
             raise ValueError("linear solver tolerances must be positive")
         if self.method not in ("bicgstab", "pcg"):
             raise ValueError(f"unknown linear solver {self.method!r}")
+        if self.operator not in ("sym", "csr"):
+            raise ValueError(f"unknown operator {self.operator!r}")
 
 
 @dataclass(frozen=True)
@@ -139,9 +145,23 @@ class NewtonReport:
     linear_stats: list = field(default_factory=list)
 
 
-def _tangent_matrix(problem, U) -> CsrMatrix:
+def _tangent_matrix(problem, U, operator="csr"):
     """K at U; cached for jacobian_constant problems (solvers.py:177-184)."""
     ws = workspace(problem)
+    if operator == "sym" and ws.has_sym:
+        key = "newton_sym"
+        if problem.jacobian_constant:
+            K = getattr(problem, "_jac_cache", None)
+            if isinstance(K, SymOperator):
+                return K
+        K = ws._cache.get(key)
+        if K is None:
+            K = SymOperator(ws)
+            ws._cache[key] = K
+        ws.jacobian_sym(problem, U, K.device_data)
+        if problem.jacobian_constant:
+            problem._jac_cache = K
+        return K
     if problem.jacobian_constant:
         K = getattr(problem, "_jac_cache", None)
         if K is None:
@@ -173,7 +193,7 @@ def _newton_device(problem, U, cfg: NewtonConfig, lin_cfg: LinearSolveConfig):
     for it in range(cfg.max_iters):
         if norms[-1] <= max(cfg.rel_tol * r0, cfg.abs_tol):
             return U, NewtonReport(norms, it, True, lin)
-        K = _tangent_matrix(problem, U)
+        K = _tangent_matrix(problem, U, lin_cfg.operator)
         lib.b200fem_scale(n, -1.0, D.ptr(R), D.ptr(rhs), stream)
         lin.append(_bicgstab_device(K, rhs, dU, False, lin_cfg))
         lib.b200fem_axpy(n, 1.0, D.ptr(dU), D.ptr(U), stream)

@@ -158,3 +158,46 @@ def _host(a, dtype):
     if isinstance(a, t.Tensor):
         a = a.detach().cpu().numpy()
     return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+class SymOperator:
+    """The tangent of a vec-3 workspace as a symmetric node-block operator (csrc SYM3).
+
+    Same linear operator as the CSR Jacobian of the workspace (identity Dirichlet rows) with
+    only the upper 3x3 node blocks stored: about half of the value bytes per matvec.  Used by
+    the Newton loop's Krylov solves; ``assemble_jacobian`` still returns the full CSR."""
+
+    def __init__(self, ws):
+        self._ws = ws
+        self._n = ws.n_dofs
+        self.device_data = D.empty(ws.sym_size())
+        self._handle = None
+
+    @property
+    def shape(self):
+        return (self._n, self._n)
+
+    def _device_handle(self):
+        if self._handle is None:
+            h = C.c_void_p()
+            raise_for(_lib.lib().b200fem_matrix_fem_sym(C.byref(h), self._ws.ctx, D.ptr(self.device_data)), None,
+                      "matrix_fem_sym")
+            self._handle = h
+        return self._handle
+
+    def matvec(self, x):
+        as_host = not D.is_device_tensor(x)
+        xd = D.to_device(x)
+        y = D.empty(self._n)
+        raise_for(_lib.lib().b200fem_matvec(self._device_handle(), D.ptr(xd), D.ptr(y)), None, "matvec")
+        return D.to_host(y) if as_host else y
+
+    __matmul__ = matvec
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and _lib._lib is not None:
+            try:
+                _lib._lib.b200fem_matrix_destroy(h)
+            except Exception:
+                pass

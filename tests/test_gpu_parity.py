@@ -376,3 +376,42 @@ def test_newton_with_pcg_matches_reference(name):
                               lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method="pcg"))
     assert rep.converged
     assert rel(U, g["U_tight"]) < 1e-8
+
+
+# ------------------------------------------------- symmetric node-block operator
+@pytest.mark.parametrize("name", ["c1", "nh_block", "j2_block", "simp_nh", "le_body"])
+def test_sym_operator_equals_csr_jacobian(name, rng):
+    from paper_2212_00964_b200.sparse import SymOperator
+    g = load_golden(name)
+    _, prob, U = build(name)
+    if "state_eps" in g:
+        prob.state = fem.QuadPointState(g["state_eps"], g["state_sig"])
+        U = g["U_test"]
+    ws = fem.workspace(prob)
+    K = fem.assemble_jacobian(prob, U)
+    S = SymOperator(ws)
+    ws.jacobian_sym(prob, D_(U), S.device_data)
+    x = rng.standard_normal(prob.n_dofs)
+    assert rel(S @ x, K @ x) < 1e-14
+    Kd = K.todense()
+    free = np.setdiff1d(np.arange(prob.n_dofs), ws.dir_dofs)
+    Kf = Kd[np.ix_(free, free)]
+    assert np.abs(Kf - Kf.T).max() <= 1e-14 * np.abs(Kf).max()  # symmetric up to in-block rounding
+
+
+def D_(U):
+    import torch
+    return torch.tensor(U, device="cuda")
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "pcg"])
+def test_newton_sym_operator_matches_csr_operator(method):
+    _, p1, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 4)))
+    _, p2, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 4)))
+    kw = dict(cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11))
+    U1, r1 = fem.newton_solve(p1, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method,
+                                                               operator="csr"), **kw)
+    U2, r2 = fem.newton_solve(p2, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method,
+                                                               operator="sym"), **kw)
+    assert r1.n_iterations == r2.n_iterations
+    assert rel(U2, U1) < 1e-9

@@ -40,12 +40,17 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--material", default="nh")
+    ap.add_argument("--operator", default="csr", choices=["csr", "sym"])
     a = ap.parse_args()
     prob = problem(a.n, a.material)
     ws = fem.workspace(prob)
     N = prob.n_dofs
     U = D.zeros(N)
     K = fem.assemble_jacobian(prob, U)
+    if a.operator == "sym":
+        from paper_2212_00964_b200.sparse import SymOperator
+        K = SymOperator(ws)
+        ws.jacobian_sym(prob, U, K.device_data)
     x = D.to_device(np.random.default_rng(0).standard_normal(N))
     y = D.empty(N)
     lib = _lib.lib()
@@ -84,7 +89,10 @@ def main():
     t_it = (t_b - t_a) / a.iters / 1e3  # marginal cost of one iteration
     e0.record()
     for _ in range(3):
-        ws.jacobian(prob, U, K.device_data)
+        if a.operator == "sym":
+            ws.jacobian_sym(prob, U, K.device_data)
+        else:
+            ws.jacobian(prob, U, K.device_data)
     e1.record()
     torch.cuda.synchronize()
     t_jac = e0.elapsed_time(e1) / 3 / 1e3
@@ -94,7 +102,10 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     t_res = e0.elapsed_time(e1) / 5 / 1e3
-    print(json.dumps({"n": a.n, "material": a.material, "nnz": nnz, "spmv_us": t * 1e6,
+    if a.operator == "sym":  # DRAM bytes of the symmetric storage: upper blocks + lower block ids
+        nsym = ws.sym_size()
+        b_fem = 8 * nsym + 4 * (nnz // 9 - nsym // 9) + 4 * (nnz // 9) + 4 * (nn + 1) * 2 + 16 * N
+    print(json.dumps({"n": a.n, "material": a.material, "operator": a.operator, "nnz": nnz, "spmv_us": t * 1e6,
                       "spmv_gbs_fem": b_fem / t / 1e9, "spmv_gbs_csr12": b_csr / t / 1e9,
                       "bicgstab_ms_per_iter": t_it * 1e3, "jacobian_ms": t_jac * 1e3,
                       "residual_ms": t_res * 1e3, "mcells": prob.mesh.n_cells / 1e6}))
