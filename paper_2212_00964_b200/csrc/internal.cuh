@@ -189,7 +189,7 @@ struct SpmvArgs {
 };
 int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
-int prepare_fem3_chunks(Matrix *m);
+int prepare_fem3_chunks(Matrix *m, int64_t node_lo = 0, int64_t node_hi = -1);
 int prepare_sym3_chunks(Matrix *m);
 
 // element kernels

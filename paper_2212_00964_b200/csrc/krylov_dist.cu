@@ -383,7 +383,14 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
   P->own_hi = own_node_hi;
   m->row_lo = own_node_lo;  // node range (FEM3/SYM3) == row range (vec-1 CSR)
   m->row_hi = own_node_hi;
-  m->use_tma = false;
+  if (m->kind == MK_FEM3 && m->use_tma) {  // bulk-copy chunks over the owned nodes only
+    if (prepare_fem3_chunks(m, own_node_lo, own_node_hi)) {
+      delete P;
+      return B200FEM_E_CUDA;
+    }
+  } else {
+    m->use_tma = false;
+  }
   P->n_peers = n_peers;
   P->peer.assign(peers, peers + n_peers);
   P->soff.assign(n_peers + 1, 0);
@@ -411,7 +418,10 @@ int b200fem_part_destroy(b200fem_part *pp) {
   cudaFree(P->recv_nodes);
   cudaFree(P->sendbuf);
   cudaFree(P->recvbuf);
-  if (P->m) P->m->row_lo = 0, P->m->row_hi = -1;
+  if (P->m) {
+    P->m->row_lo = 0, P->m->row_hi = -1;
+    if (P->m->use_tma) prepare_fem3_chunks(P->m);
+  }
   delete P;
   return 0;
 }

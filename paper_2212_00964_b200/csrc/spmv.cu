@@ -433,14 +433,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
 
 // Pack consecutive nodes into chunks whose values + neighbour ids fit one stage
 // (with 16-byte alignment slack), at most one node per consumer warp.
-int prepare_fem3_chunks(Matrix *m) {
+int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
   const int64_t nn = m->n / 3;
+  if (hi < 0) hi = nn;
   std::vector<int32_t> ptr(nn + 1);
   if (cudaMemcpy(ptr.data(), m->nbr_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
     return B200FEM_E_CUDA;
-  std::vector<int32_t> ch{0};
-  int64_t start = 0;
-  for (int64_t n = 0; n < nn; ++n) {
+  cudaFree(m->chunk_node);
+  m->chunk_node = nullptr;
+  m->use_tma = false;
+  std::vector<int32_t> ch{(int32_t)lo};
+  int64_t start = lo;
+  for (int64_t n = lo; n < hi; ++n) {
     const int64_t nb = ptr[n + 1] - ptr[start];
     const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= kTmaConsumers;
     if (!fits) {
@@ -449,7 +453,7 @@ int prepare_fem3_chunks(Matrix *m) {
       start = n;
     }
   }
-  ch.push_back((int32_t)nn);
+  ch.push_back((int32_t)hi);
   m->n_chunks = (int)ch.size() - 1;
   if (dalloc(&m->chunk_node, ch.size()) != cudaSuccess) return B200FEM_E_CUDA;
   if (cudaMemcpy(m->chunk_node, ch.data(), ch.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -691,7 +695,7 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
   RedScratch r = red ? *red : RedScratch{};
   const bool full = m->row_hi < 0;
-  if (m->kind == MK_FEM3 && m->use_tma && full) {
+  if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
