@@ -364,6 +364,7 @@ def run_ours(args):
                      "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,
                      "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6},
         "newton": {"linear_method": args.linear, "iterations": rep.n_iterations,
+                   "phase_s": getattr(rep, "timings", None),
                    "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
                    "per_step_ms": per_step},
         "alt_linear": alt,

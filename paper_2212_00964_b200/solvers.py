@@ -143,6 +143,8 @@ class NewtonReport:
     n_iterations: int
     converged: bool
     linear_stats: list = field(default_factory=list)
+    # device time per phase (CUDA events on the solve's stream): residual, jacobian, linear
+    timings: dict = field(default_factory=dict)
 
 
 def _tangent_matrix(problem, U, operator="csr"):
@@ -178,6 +180,24 @@ def _tangent_matrix(problem, U, operator="csr"):
     return K
 
 
+class _PhaseTimer:
+    """CUDA-event phase accounting (no host synchronisation added)."""
+
+    def __init__(self):
+        self.events = []
+
+    def mark(self, phase):
+        ev = D.torch().cuda.Event(enable_timing=True)
+        ev.record()
+        self.events.append((phase, ev))
+
+    def totals(self):
+        out = {}
+        for (ph, a), (_, b) in zip(self.events, self.events[1:]):
+            out[ph] = out.get(ph, 0.0) + a.elapsed_time(b) / 1e3
+        return out
+
+
 def _newton_device(problem, U, cfg: NewtonConfig, lin_cfg: LinearSolveConfig):
     """Newton on device vectors; U (CUDA tensor) is updated in place."""
     ws = workspace(problem)
@@ -187,19 +207,29 @@ def _newton_device(problem, U, cfg: NewtonConfig, lin_cfg: LinearSolveConfig):
     dU = D.empty(n)
     lib = _lib.lib()
     stream = D.stream()
+    tm = _PhaseTimer()
+    tm.mark("residual_s")
     norms = [ws.residual(problem, U, R)]
     r0 = norms[0]
     lin = []
+
+    def report(its, ok):
+        tm.mark("end")
+        return NewtonReport(norms, its, ok, lin, tm.totals())
+
     for it in range(cfg.max_iters):
         if norms[-1] <= max(cfg.rel_tol * r0, cfg.abs_tol):
-            return U, NewtonReport(norms, it, True, lin)
+            return U, report(it, True)
+        tm.mark("jacobian_s")
         K = _tangent_matrix(problem, U, lin_cfg.operator)
+        tm.mark("linear_s")
         lib.b200fem_scale(n, -1.0, D.ptr(R), D.ptr(rhs), stream)
         lin.append(_bicgstab_device(K, rhs, dU, False, lin_cfg))
         lib.b200fem_axpy(n, 1.0, D.ptr(dU), D.ptr(U), stream)
+        tm.mark("residual_s")
         norms.append(ws.residual(problem, U, R))
     if norms[-1] <= max(cfg.rel_tol * r0, cfg.abs_tol):
-        return U, NewtonReport(norms, cfg.max_iters, True, lin)
+        return U, report(cfg.max_iters, True)
     raise NonConvergenceError(
         f"Newton did not converge in {cfg.max_iters} iterations "
         f"(residual history {['%.3e' % v for v in norms]})", residual_norms=norms)
