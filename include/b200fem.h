@@ -125,6 +125,21 @@ int b200fem_volume_average_flux(b200fem_ctx *ctx, const double *U_dev, double *o
 /* J2 state commit eps <- sym grad u, sig <- return map (problems.py:155-163) */
 int b200fem_commit_state(b200fem_ctx *ctx, const double *U_dev);
 
+/* ---- adjoint half ---- */
+/* param_vjp: out = w_eff^T dR/dtheta at U (assembly.py:303-341); w_eff zeroes the Dirichlet
+ * rows.  SIMP ctx: out has n_cells entries (theta: n_cells); design-source ctx: n_nodes
+ * (theta: n_nodes, U unused).  theta is the design vector to differentiate at (not the one
+ * bound by set_theta). */
+int b200fem_param_vjp(b200fem_ctx *ctx, const double *U_dev, const double *theta_dev, const double *w_dev,
+                      double *out_dev, b200fem_error *err);
+/* transpose_fem: values of A^T on this ctx's (structurally symmetric) pattern; a pure
+ * permutation of data_dev, bit-identical to CsrMatrix.transpose (sparse.py:53-62). */
+int b200fem_transpose_fem(b200fem_ctx *ctx, const double *data_dev, double *data_t_dev);
+/* csr_transpose: generic CSR transpose (stable by column, sparse.py:53-62); synchronous. */
+int b200fem_csr_transpose(int64_t n, int64_t nnz, const int32_t *indptr_dev, const int32_t *indices_dev,
+                          const double *data_dev, int32_t *indptr_t_dev, int32_t *indices_t_dev,
+                          double *data_t_dev, void *stream);
+
 /* ---- sparse operators (sparse.py:15-51, kernels.py:37-47) ---- */
 /* FEM matrix on this ctx's pattern (uses the node-blocked index, no indices array) */
 int b200fem_matrix_fem(b200fem_matrix **out, b200fem_ctx *ctx, const double *data_dev);
@@ -187,6 +202,7 @@ int b200fem_dist_dot(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, d
 
 /* ---- small vector helpers (deterministic) ---- */
 int b200fem_norm2(const double *x_dev, int64_t n, double *out_host, void *stream);
+int b200fem_dot(const double *x_dev, const double *y_dev, int64_t n, double *out_host, void *stream);
 int b200fem_gather_sum(const double *x_dev, const int64_t *idx_dev, int64_t n, double *out_host,
                        void *stream);
 int b200fem_axpy(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);

@@ -76,6 +76,9 @@ SIGNATURES = {
     "b200fem_qp_flux": (C.c_int, [_vp, _vp, _vp, _perr]),
     "b200fem_volume_average_flux": (C.c_int, [_vp, _vp, _vp, _perr]),
     "b200fem_commit_state": (C.c_int, [_vp, _vp]),
+    "b200fem_param_vjp": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _perr]),
+    "b200fem_transpose_fem": (C.c_int, [_vp, _vp, _vp]),
+    "b200fem_csr_transpose": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "b200fem_matrix_fem": (C.c_int, [C.POINTER(_vp), _vp, _vp]),
     "b200fem_matrix_csr": (C.c_int, [C.POINTER(_vp), _i64, _i64, _vp, _vp, _vp, _vp]),
     "b200fem_ctx_sym_size": (C.c_int, [_vp, _pi64]),
@@ -99,6 +102,7 @@ SIGNATURES = {
     "b200fem_dist_halo": (C.c_int, [_vp, _i32, _vp, _vp]),
     "b200fem_dist_dot": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _pf64]),
     "b200fem_norm2": (C.c_int, [_vp, _i64, _pf64, _vp]),
+    "b200fem_dot": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_gather_sum": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_axpy": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
     "b200fem_scale": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),

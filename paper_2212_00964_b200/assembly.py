@@ -28,7 +28,7 @@ from .sparse import CsrMatrix
 
 __all__ = ["DirichletSpec", "NeumannSpec", "ConflictingConstraintError", "KernelEvaluationError",
            "UnsupportedKernelError", "workspace", "assemble_residual", "assemble_jacobian",
-           "impose_dirichlet_residual"]
+           "impose_dirichlet_residual", "assemble_param_vjp"]
 
 
 @dataclass(frozen=True)
@@ -256,6 +256,13 @@ class DeviceWorkspace:
                                              D.ptr(sym), C.byref(err))
         raise_for(st, err, "jacobian_sym")
 
+    def param_vjp(self, problem, U, theta, w, out):
+        """out <- w_eff^T dR/dtheta at (U, theta) on the device (assembly.py:303-341)."""
+        err = _lib.Error()
+        st = _lib.lib().b200fem_param_vjp(self.ctx, D.ptr(U) if U is not None else None, D.ptr(theta), D.ptr(w),
+                                          D.ptr(out), C.byref(err))
+        raise_for(st, err, "param_vjp")
+
     def qp_flux(self, problem, U):
         self.sync(problem)
         out = D.empty(self.n_cells * 8 * self.vec * 3)
@@ -375,3 +382,28 @@ def assemble_jacobian(problem, U) -> CsrMatrix:
     data = D.empty(ws.nnz)
     ws.jacobian(problem, Ud, data)
     return CsrMatrix._from_workspace(ws, data)
+
+
+def assemble_param_vjp(problem, U, theta, w):
+    """w^T (dR/dtheta) accumulated into design space (assembly.py:303-341).
+
+    Constrained residual rows are design-independent: their w entries are zeroed.  SIMP
+    problems return one entry per cell, a Poisson design source one per node.  Host inputs
+    give a host array (drop-in); CUDA tensors stay on the device."""
+    ws = workspace(problem)
+    if problem.design_layout is None:
+        raise ValueError("problem has no design parameters bound")
+    as_host = not D.is_device_tensor(w)
+    Ud = D.to_device(U)
+    if tuple(Ud.shape) != (problem.n_dofs,):
+        raise ValueError(f"U must have shape ({problem.n_dofs},), got {tuple(Ud.shape)}")
+    th = D.to_device(theta)
+    if tuple(th.shape) != (problem.n_design,):
+        raise ValueError(f"theta must have shape ({problem.n_design},), got {tuple(th.shape)}")
+    wd = D.to_device(w)
+    if tuple(wd.shape) != (problem.n_dofs,):
+        raise ValueError(f"w must have shape ({problem.n_dofs},), got {tuple(wd.shape)}")
+    out = D.empty(problem.n_design)
+    ws.sync(problem)
+    ws.param_vjp(problem, Ud, th, wd, out)
+    return D.to_host(out) if as_host else out

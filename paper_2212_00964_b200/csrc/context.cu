@@ -710,6 +710,19 @@ int b200fem_norm2(const double *x, int64_t n, double *out_host, void *stream) {
   return st;
 }
 
+int b200fem_dot(const double *x, const double *y, int64_t n, double *out_host, void *stream) {
+  RedScratch r{};
+  if (red_alloc(&r)) return B200FEM_E_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st = launch_dot(x, y, n, &r, s);
+  double v = 0.0;
+  if (!st && cudaMemcpyAsync(&v, r.result, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess) st = B200FEM_E_CUDA;
+  if (!st && cudaStreamSynchronize(s) != cudaSuccess) st = B200FEM_E_CUDA;
+  red_free(&r);
+  *out_host = v;
+  return st;
+}
+
 int b200fem_gather_sum(const double *x, const int64_t *idx, int64_t n, double *out_host, void *stream) {
   RedScratch r{};
   if (red_alloc(&r)) return B200FEM_E_CUDA;

@@ -340,6 +340,105 @@ __global__ void __launch_bounds__(kThreads, 2) k_residual(ElemArgs a, int64_t n,
   }
 }
 
+// ------------------------------------------------------------- design VJP
+// out = w_eff^T dR/dtheta (assembly.py:303-341), w_eff = w with the Dirichlet rows zeroed
+// (they do not depend on theta).  SIMP (element layout, problems.py:166-170): the flux is
+// theta_e^p sigma(grad u), so dR_e/dtheta_e = p theta_e^(p-1) * (unscaled element
+// residual) and out[e] = that dotted with w_e.  8 lanes per cell as in k_residual.
+template <int MAT>
+__global__ void __launch_bounds__(kThreads, 2) k_vjp_simp(ElemArgs a, int64_t n, const double *__restrict__ th,
+                                                          const double *__restrict__ w,
+                                                          const uint8_t *__restrict__ dflag, double *__restrict__ out) {
+  __shared__ double sX[kWarps][4][8][3];
+  __shared__ double sU[kWarps][4][8][3];
+  __shared__ double sW[kWarps][4][8][3];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, slot = lane >> 3, q = lane & 7;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
+    const int64_t idx = base + slot;
+    const bool valid = idx < n;
+    const int64_t e = valid ? idx : base;
+    const int node = a.cells[e * 8 + q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int64_t dof = (int64_t)node * 3 + d;
+      sX[wp][slot][q][d] = a.coords[dof];
+      sU[wp][slot][q][d] = a.U[dof];
+      sW[wp][slot][q][d] = (dflag && dflag[dof]) ? 0.0 : w[dof];
+    }
+    __syncwarp();
+    double G[8][3];
+    const double jxw = qp_geometry(sX[wp][slot], q, G);
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gu[v][d] = fma(sU[wp][slot][k][v], G[k][d], gu[v][d]);
+    double P[3][3], detF = 1.0;
+    const bool ok = flux_at<MAT>(gu, a.mp, nullptr, nullptr, P, detF);
+    if (valid) {
+      const unsigned long long key = (unsigned long long)e * 8 + q;
+      if (!ok) {
+        atomicMin(&a.derr->inv_def, key);
+        atomicMin(&a.derr->min_detF, ord_bits(detF));
+      } else if (!all_finite(P, 3)) {
+        atomicMin(&a.derr->nonfin_v, key);
+      }
+    }
+    const double sc = jxw * (a.mp.penalty * pow(th[e], a.mp.penalty - 1.0));
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+        acc = fma(sc * (P[v][0] * G[k][0] + P[v][1] * G[k][1] + P[v][2] * G[k][2]), sW[wp][slot][k][v], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (valid && q == 0) out[e] = acc;
+    __syncwarp();
+  }
+}
+
+// Poisson design source (node layout, problems.py:125-130): b_q = sum_k theta_k N_k(q)
+// enters R_e,i as -sum_q b_q N_i(q) JxW_q, so the VJP of cell e at its local node k is
+// -sum_q N_k(q) JxW_q (sum_i N_i(q) w_i); written per (cell, local node) for the ordered
+// node gather (the reference's scatter_add over cells[sl].ravel()).
+__global__ void __launch_bounds__(kThreads, 2) k_vjp_source(ElemArgs a, int64_t n, const double *__restrict__ w,
+                                                            const uint8_t *__restrict__ dflag,
+                                                            double *__restrict__ Re) {
+  __shared__ double sX[kWarps][4][8][3];
+  __shared__ double sW[kWarps][4][8];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, slot = lane >> 3, q = lane & 7;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
+    const int64_t idx = base + slot;
+    const bool valid = idx < n;
+    const int64_t e = valid ? idx : base;
+    const int node = a.cells[e * 8 + q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sX[wp][slot][q][d] = a.coords[(int64_t)node * 3 + d];
+    sW[wp][slot][q] = (dflag && dflag[node]) ? 0.0 : w[node];
+    __syncwarp();
+    double G[8][3];
+    const double jxw = qp_geometry(sX[wp][slot], q, G);
+    double wq = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wq = fma(c_N[q][k], sW[wp][slot][k], wq);
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = -(c_N[q][k] * wq * jxw);
+    double mine[1];
+    reduce_scatter8<1>(r, q, mine);
+    if (valid) Re[e * 8 + q] = mine[0];
+    __syncwarp();
+  }
+}
+
 // Ordered gather (assembly.py:256 semantics): R[n] = sum over the node's incident cells in
 // ascending cell id of R_e[e, a(n,e)] -- the reference's accumulation order, no atomics.
 template <int VEC>
@@ -939,6 +1038,35 @@ int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int app
   return 0;
 }
 
+// Design VJP (assembly.py:303-341): SIMP -> one value per cell; design source -> per-cell
+// local-node values gathered per node in ascending cell order.
+int launch_param_vjp(Ctx *c, const double *U, const double *theta, const double *w, double *out,
+                     b200fem_error *err) {
+  cudaStream_t s = c->stream;
+  const ElemArgs a = make_args(c, U);
+  const int g = grid_cap(c->n_cells, kWarps * 4);
+  if (c->flags & B200FEM_FLAG_SIMP) {
+    if (c->vec != 3 || !U) return B200FEM_E_INVALID;
+    switch (c->material) {
+      case B200FEM_MAT_LE: k_vjp_simp<B200FEM_MAT_LE><<<g, kThreads, 0, s>>>(a, c->n_cells, theta, w, c->dir_flag, out); break;
+      case B200FEM_MAT_NH: k_vjp_simp<B200FEM_MAT_NH><<<g, kThreads, 0, s>>>(a, c->n_cells, theta, w, c->dir_flag, out); break;
+      default: return B200FEM_E_UNSUPPORTED;
+    }
+    count_launch();
+  } else if (c->flags & B200FEM_FLAG_DESIGN_SOURCE) {
+    if (c->vec != 1) return B200FEM_E_INVALID;
+    if (ensure_scratch(c, (size_t)c->n_cells * 8, err)) return B200FEM_E_CUDA;
+    k_vjp_source<<<g, kThreads, 0, s>>>(a, c->n_cells, w, c->dir_flag, c->scratch);
+    k_residual_gather<1><<<grid_cap(c->n_nodes, kThreads), kThreads, 0, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->scratch,
+                                                                            c->n_nodes, 0.0, nullptr, nullptr, out);
+    count_launch(2);
+  } else {
+    return B200FEM_E_INVALID;
+  }
+  B200_CUDA_E(cudaGetLastError(), err);
+  return fetch_element_errors(c, err, false);  // synchronises the stream
+}
+
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
 int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym) {
@@ -1031,6 +1159,13 @@ int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U, double *data, double
   Ctx *c = (Ctx *)ctx;
   if (c->vec != 3 || !sym) return B200FEM_E_INVALID;
   return launch_jacobian(c, U, data, err, sym);
+}
+
+int b200fem_param_vjp(b200fem_ctx *ctx, const double *U, const double *theta, const double *w, double *out,
+                      b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  if (!ctx || !theta || !w || !out) return B200FEM_E_INVALID;
+  return launch_param_vjp((Ctx *)ctx, U, theta, w, out, err);
 }
 
 int b200fem_qp_flux(b200fem_ctx *ctx, const double *U, double *out, b200fem_error *err) {

@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstring>
+
 #include "internal.cuh"
 
 namespace b200 {
@@ -311,14 +313,35 @@ __device__ __forceinline__ RowPre row_pre_from(const double *e0, const double *e
   return p;
 }
 
+// x_m of neighbour node m (3 doubles at 24 m).  XV=0: three 8-byte loads; XV=1: one
+// 16-byte load of the aligned pair plus one 8-byte load (x must be 16-byte aligned);
+// XV=2 (diagnostic only, wrong results): no gather, to separate its cost.
+template <int XV>
+__device__ __forceinline__ void load_x3(const double *__restrict__ x, int m, double &x0, double &x1, double &x2) {
+  const double *__restrict__ xm = x + 3 * (int64_t)m;
+  if (XV == 0) {
+    x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+  } else if (XV == 1) {
+    const int odd = m & 1;
+    const double2 v = __ldg(reinterpret_cast<const double2 *>(xm + odd));
+    const double sc = __ldg(xm + (odd ? 0 : 2));
+    x0 = odd ? sc : v.x;
+    x1 = odd ? v.x : v.y;
+    x2 = odd ? v.y : sc;
+  } else {
+    x0 = 1.0, x1 = 0.5, x2 = 0.25;
+  }
+}
+
 // One node's three row sums from a value block `sv` (stage or global) and its neighbour ids.
+template <int XV = 0>
 __device__ __forceinline__ void node_rows(const double *sv, const int32_t *sn, int cnt, const double *__restrict__ x,
                                           int lane, double &y0, double &y1, double &y2) {
   const int L = 3 * cnt;
   for (int j = lane; j < cnt; j += 32) {
     const int m = sn[j];
-    const double *__restrict__ xm = x + 3 * (int64_t)m;
-    const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
+    double x0, x1, x2;
+    load_x3<XV>(x, m, x0, x1, x2);
     const double *r0 = sv + 3 * j;
     y0 = fma(r0[2], x2, fma(r0[1], x1, fma(r0[0], x0, y0)));
     y1 = fma(r0[L + 2], x2, fma(r0[L + 1], x1, fma(r0[L], x0, y1)));
@@ -326,7 +349,7 @@ __device__ __forceinline__ void node_rows(const double *sv, const int32_t *sn, i
   }
 }
 
-template <int MODE>
+template <int MODE, int XV>
 __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t *__restrict__ nbr_ptr,
                                                                  const int32_t *__restrict__ nbr,
                                                                  const double *__restrict__ data,
@@ -410,11 +433,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
       double y0 = 0.0, y1 = 0.0, y2 = 0.0;
       if (has) {
         if (!tail)
-          node_rows(reinterpret_cast<const double *>(stage + (72ull * pA - vb0)),
+          node_rows<XV>(reinterpret_cast<const double *>(stage + (72ull * pA - vb0)),
                     reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0)), cA, a.x, lane, y0, y1,
                     y2);
         else
-          node_rows(data + 9 * pA, nbr + pA, cA, a.x, lane, y0, y1, y2);
+          node_rows<XV>(data + 9 * pA, nbr + pA, cA, a.x, lane, y0, y1, y2);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);  // stage reads done; the producer may refill it
@@ -429,6 +452,27 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t 
     if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
       spmv_stage<MODE>(a.sc, tot);
   }
+}
+
+template <int XV>
+static void set_tma_attr() {
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PLAIN, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_R0, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_TT, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_RESIDUAL, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PQ, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_CGRES, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+}
+
+// x-gather variant of the bulk-copy kernel (B200FEM_SPMV_X = "vec" | "none"; "none" is a
+// diagnostic that skips the gather and computes wrong results).
+static int tma_x_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("B200FEM_SPMV_X");
+    v = (e && !strcmp(e, "vec")) ? 1 : (e && !strcmp(e, "none")) ? 2 : 0;
+  }
+  return v;
 }
 
 // Pack consecutive nodes into chunks whose values + neighbour ids fit one stage
@@ -460,12 +504,9 @@ int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
     return B200FEM_E_CUDA;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-    cudaFuncSetAttribute(k_spmv_fem3_tma<SP_CGRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    set_tma_attr<0>();
+    set_tma_attr<1>();
+    set_tma_attr<2>();
     attr = true;
   }
   m->use_tma = true;
@@ -700,8 +741,14 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = std::min(sms, m->n_chunks);
-    k_spmv_fem3_tma<MODE><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
-                                                                  m->n_chunks, m->nnz / 9, m->n, a, r);
+    switch (tma_x_variant()) {
+      case 1: k_spmv_fem3_tma<MODE, 1><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
+                                                                                m->n_chunks, m->nnz / 9, m->n, a, r); break;
+      case 2: k_spmv_fem3_tma<MODE, 2><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
+                                                                                m->n_chunks, m->nnz / 9, m->n, a, r); break;
+      default: k_spmv_fem3_tma<MODE, 0><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
+                                                                                 m->n_chunks, m->nnz / 9, m->n, a, r);
+    }
   } else if (m->kind == MK_SYM3 && m->use_tma && full) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

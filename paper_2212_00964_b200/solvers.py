@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .assembly import workspace
+from .assembly import assemble_jacobian, workspace
 from .errors import BreakdownError, LinearSolverError, NonConvergenceError, raise_for
 from .mesh import BoundaryLocator, locate_nodes
 from .sparse import CsrMatrix, SymOperator
@@ -233,6 +233,21 @@ def _newton_device(problem, U, cfg: NewtonConfig, lin_cfg: LinearSolveConfig):
     raise NonConvergenceError(
         f"Newton did not converge in {cfg.max_iters} iterations "
         f"(residual history {['%.3e' % v for v in norms]})", residual_norms=norms)
+
+
+def tangent_transpose(problem, U) -> CsrMatrix:
+    """Transpose of the (Dirichlet-modified) tangent at U (solvers.py:187-195), on the device;
+    cached for jacobian_constant problems."""
+    if problem.jacobian_constant:
+        cached = getattr(problem, "_jac_t_cache", None)
+        if cached is None:
+            K = _tangent_matrix(problem, D.to_device(U), "csr")
+            if not isinstance(K, CsrMatrix):  # a symmetric-storage cache: assemble the CSR
+                K = assemble_jacobian(problem, U)
+            cached = K.transpose()
+            problem._jac_t_cache = cached
+        return cached
+    return assemble_jacobian(problem, U).transpose()
 
 
 def newton_solve(problem, U0=None, cfg: NewtonConfig = NewtonConfig(),

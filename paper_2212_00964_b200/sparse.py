@@ -147,6 +147,28 @@ class CsrMatrix:
         out[rows, self.indices] = self.data
         return out
 
+    def transpose(self) -> "CsrMatrix":
+        """Explicit transpose on the device (sparse.py:53-62: stable by column).
+
+        A workspace matrix keeps its (structurally symmetric) pattern and only permutes the
+        values (csrc/transpose.cu); a generic CSR goes through a stable radix sort."""
+        lib = _lib.lib()
+        if self._ws is not None:
+            data_t = D.empty(self._ws.nnz)
+            raise_for(lib.b200fem_transpose_fem(self._ws.ctx, D.ptr(self.device_data), D.ptr(data_t)), None,
+                      "transpose_fem")
+            return CsrMatrix._from_workspace(self._ws, data_t)
+        t = D.torch()
+        n, nnz = self._n, int(self._h_indices.shape[0])
+        ip = D.to_device(self._h_indptr, t.int32)
+        ix = D.to_device(self._h_indices, t.int32)
+        ip_t = D.empty(n + 1, t.int32)
+        ix_t = D.empty(max(nnz, 1), t.int32)
+        d_t = D.empty(max(nnz, 1))
+        raise_for(lib.b200fem_csr_transpose(n, nnz, D.ptr(ip), D.ptr(ix), D.ptr(self.device_data), D.ptr(ip_t),
+                                            D.ptr(ix_t), D.ptr(d_t), D.stream()), None, "csr_transpose")
+        return CsrMatrix(D.to_host(ip_t), D.to_host(ix_t)[:nnz], d_t[:nnz])
+
     def copy_structure(self) -> "CsrMatrix":
         if self._ws is not None:
             return CsrMatrix._from_workspace(self._ws, D.zeros(self._ws.nnz))

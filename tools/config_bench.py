@@ -112,15 +112,8 @@ if __name__ == "__main__":
     ap.add_argument("--only", default="c1,c2,c4,c5")
     ap.add_argument("--c4n", type=int, default=40)
     a = ap.parse_args()
-    res = []
+    runs = {"c1": lambda: [c1()], "c2": lambda: [c2()], "c4": lambda: [c4(a.c4n)],
+            "c5": lambda: [c5("bicgstab"), c5("pcg")]}
     for name in a.only.split(","):
-        if name == "c1":
-            res.append(c1())
-        elif name == "c2":
-            res.append(c2())
-        elif name == "c4":
-            res.append(c4(a.c4n))
-        elif name == "c5":
-            res.append(c5("bicgstab"))
-            res.append(c5("pcg"))
-        print(json.dumps(res[-1]), flush=True)
+        for r in runs[name]():
+            print(json.dumps(r), flush=True)
