@@ -193,6 +193,8 @@ class _PhaseTimer:
 
     def totals(self):
         out = {}
+        if self.events:
+            self.events[-1][1].synchronize()  # the closing mark may still be in flight
         for (ph, a), (_, b) in zip(self.events, self.events[1:]):
             out[ph] = out.get(ph, 0.0) + a.elapsed_time(b) / 1e3
         return out
