@@ -251,3 +251,12 @@ def test_optimize_lbfgs_on_poisson_inference(rng):
     obj = _poisson_obj(prob, obs, rng.standard_normal(obs.size) * 0.01)
     theta, hist = optimize(obj.value_and_gradient, np.zeros(mesh.n_nodes), max_iters=30, gtol=1e-12)
     assert hist.objective[-1] < 1e-3 * hist.objective[0]
+
+
+@pytest.mark.parametrize("name", DESIGN)
+def test_adjoint_pcg_split_matches_reference(name):
+    g = load_golden(f"{name}_adjoint")
+    _, prob, _ = build(name)
+    cfg = fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method="pcg")
+    lam = adjoint_solve(prob, g["U_tight"], g["dj_du"], lin_cfg=cfg)
+    assert rel(lam, g["lam_tight"]) < 1e-8
