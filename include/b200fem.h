@@ -200,6 +200,31 @@ int b200fem_dist_halo(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, 
 int b200fem_dist_dot(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *x,
                      double *const *y, double *out_host);
 
+/* ---- design loop (inverse.py:186-346) ---- */
+typedef struct b200fem_filter b200fem_filter;
+/* density filter: hat weights max(0, r - |c_j - c_i|) over element centroids, row-normalised
+ * (inverse.py:204-228, the reference builds it with a k-d tree).  cells: (n_cells, 8) int32. */
+int b200fem_filter_create(b200fem_filter **out, int64_t n_cells, const double *coords_dev,
+                          const int32_t *cells_dev, double radius, void *stream);
+int b200fem_filter_info(const b200fem_filter *f, int64_t *n, int64_t *nnz);
+/* copy the filter CSR into caller buffers (n+1, nnz, nnz) */
+int b200fem_filter_copy(const b200fem_filter *f, int32_t *indptr_dev, int32_t *indices_dev, double *data_dev);
+/* y = H (v [* mul]) [/ max(div, floor)]: filt(field) and filter_sensitivities (inverse.py:186-234) */
+int b200fem_filter_apply(const b200fem_filter *f, const double *v_dev, const double *mul_dev /* nullable */,
+                         const double *div_dev /* nullable */, double floor_value, double *y_dev);
+int b200fem_filter_destroy(b200fem_filter *f);
+/* one MMA step for a single linear constraint (inverse.py:260-346).  lower/upper: previous
+ * asymptotes in (when use_history), new asymptotes out.  Synchronous. */
+int b200fem_mma_update(int64_t n, const double *x_dev, const double *dj_dev, double g_value,
+                       const double *g_grad_dev, const double *lb_dev, const double *ub_dev, double *lower_dev,
+                       double *upper_dev, const double *x_prev_dev, const double *x_prev2_dev,
+                       int32_t use_history, double asym_init, double asym_expand, double asym_shrink,
+                       double move_limit, double *x_new_dev, void *stream);
+/* relative L2 field error terms by quadrature (inverse.py:45-56): out_host = {sum (u_p-u_t)^2 JxW,
+ * sum u_t^2 JxW} for nodal scalar fields on (n_cells, 8) int32 cells. */
+int b200fem_l2_field_error(int64_t n_cells, const double *coords_dev, const int32_t *cells_dev,
+                           const double *u_pred_dev, const double *u_true_dev, double *out_host, void *stream);
+
 /* ---- small vector helpers (deterministic) ---- */
 int b200fem_norm2(const double *x_dev, int64_t n, double *out_host, void *stream);
 int b200fem_dot(const double *x_dev, const double *y_dev, int64_t n, double *out_host, void *stream);

@@ -103,6 +103,14 @@ SIGNATURES = {
     "b200fem_dist_dot": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _pf64]),
     "b200fem_norm2": (C.c_int, [_vp, _i64, _pf64, _vp]),
     "b200fem_dot": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
+    "b200fem_filter_create": (C.c_int, [C.POINTER(_vp), _i64, _vp, _vp, C.c_double, _vp]),
+    "b200fem_filter_info": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
+    "b200fem_filter_copy": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "b200fem_filter_apply": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp]),
+    "b200fem_filter_destroy": (C.c_int, [_vp]),
+    "b200fem_mma_update": (C.c_int, [_i64, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                     C.c_double, C.c_double, C.c_double, C.c_double, _vp, _vp]),
+    "b200fem_l2_field_error": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _pf64, _vp]),
     "b200fem_gather_sum": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_axpy": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
     "b200fem_scale": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),

@@ -439,6 +439,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_vjp_source(ElemArgs a, int64_t 
   }
 }
 
+// ------------------------------------------------------------- L2 field error
+// inverse.py:45-56: per quadrature point d = sum_k N_k(q) u_k for the predicted and true
+// nodal fields; sums of (d_p - d_t)^2 JxW and d_t^2 JxW (deterministic block reduction).
+__global__ void __launch_bounds__(kThreads) k_l2_error(const double *__restrict__ X, const int32_t *__restrict__ cells,
+                                                       int64_t n, const double *__restrict__ up,
+                                                       const double *__restrict__ ut, RedScratch red,
+                                                       double *__restrict__ out) {
+  __shared__ double sX[kWarps][4][8][3];
+  __shared__ double sP[kWarps][4][8], sT[kWarps][4][8];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, slot = lane >> 3, q = lane & 7;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
+    const int64_t idx = base + slot;
+    const bool valid = idx < n;
+    const int64_t e = valid ? idx : base;
+    const int node = cells[e * 8 + q];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sX[wp][slot][q][d] = X[(int64_t)node * 3 + d];
+    sP[wp][slot][q] = up[node];
+    sT[wp][slot][q] = ut[node];
+    __syncwarp();
+    double G[8][3];
+    const double jxw = qp_geometry(sX[wp][slot], q, G);
+    double dp = 0.0, dt = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dp = fma(c_N[q][k], sP[wp][slot][k], dp);
+      dt = fma(c_N[q][k], sT[wp][slot][k], dt);
+    }
+    if (valid) {
+      const double df = dp - dt;
+      acc[0] = fma(df * df, jxw, acc[0]);
+      acc[1] = fma(dt * dt, jxw, acc[1]);
+    }
+    __syncwarp();
+  }
+  double tot[2];
+  if (block_partials_and_finish<2>(acc, red, tot) && threadIdx.x == 0) out[0] = tot[0], out[1] = tot[1];
+}
+
 // Ordered gather (assembly.py:256 semantics): R[n] = sum over the node's incident cells in
 // ascending cell id of R_e[e, a(n,e)] -- the reference's accumulation order, no atomics.
 template <int VEC>
@@ -1166,6 +1208,28 @@ int b200fem_param_vjp(b200fem_ctx *ctx, const double *U, const double *theta, co
   if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
   if (!ctx || !theta || !w || !out) return B200FEM_E_INVALID;
   return launch_param_vjp((Ctx *)ctx, U, theta, w, out, err);
+}
+
+int b200fem_l2_field_error(int64_t n_cells, const double *coords, const int32_t *cells, const double *up,
+                           const double *ut, double *out_host, void *stream) {
+  if (n_cells < 0 || !out_host) return B200FEM_E_INVALID;
+  out_host[0] = out_host[1] = 0.0;
+  if (n_cells == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  RedScratch red{};
+  double *d = nullptr;
+  int st = B200FEM_E_CUDA;
+  if (!red_alloc(&red) && dalloc(&d, 2) == cudaSuccess) {
+    const int g = std::min(kRedBlocks, grid_cap(n_cells, kWarps * 4));
+    k_l2_error<<<g, kThreads, 0, s>>>(coords, cells, n_cells, up, ut, red, d);
+    count_launch();
+    if (cudaMemcpyAsync(out_host, d, 2 * sizeof(double), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+        cudaStreamSynchronize(s) == cudaSuccess)
+      st = 0;
+  }
+  cudaFree(d);
+  red_free(&red);
+  return st;
 }
 
 int b200fem_qp_flux(b200fem_ctx *ctx, const double *U, double *out, b200fem_error *err) {
