@@ -39,6 +39,8 @@ def to_device(x, dtype=None, copy=False):
         y = y.contiguous()
         return y.clone() if (copy and y.data_ptr() == x.data_ptr()) else y
     arr = np.ascontiguousarray(np.asarray(x), dtype=_np_dtype(dt))
+    if not arr.flags.writeable:  # e.g. np.broadcast_to views
+        arr = arr.copy()
     return t.from_numpy(arr).to(device(), non_blocking=False)
 
 

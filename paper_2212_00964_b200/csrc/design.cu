@@ -500,30 +500,34 @@ int b200fem_mma_update(int64_t n, const double *x, const double *dj, double g_va
   if (use_history && (!x_prev || !x_prev2)) return B200FEM_E_INVALID;
   if (n == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  double *work = nullptr;
-  MmaCtl *ctl = nullptr;
-  RedScratch red{};
-  int st = B200FEM_E_CUDA;
-  do {
-    if (dalloc(&work, 4 * n) || dalloc(&ctl, 1) || red_alloc(&red)) break;
-    MmaCtl h{};
-    h.g_value = g_value;
-    if (cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s)) break;
-    MmaArgs a{x, dj, g_grad, lb, ub, x_prev, x_prev2, lower, upper, work, work + n, work + 2 * n, work + 3 * n,
-              x_new, asym_init, asym_expand, asym_shrink, move_limit, use_history};
-    const int gv = grid_n(n), gr = std::min(kRedBlocks, gv);
-    k_mma_absmax<<<gv, kThreads, 0, s>>>(n, dj, ctl);
-    k_mma_prep<<<gv, kThreads, 0, s>>>(n, a, ctl);
-    for (int e = 0; e < 1 + 41 + 100; ++e) k_mma_eval<false><<<gr, kThreads, 0, s>>>(n, a, ctl, red);
-    k_mma_eval<true><<<gv, kThreads, 0, s>>>(n, a, ctl, red);
-    count_launch(2 + 142 + 1);
-    if (cudaStreamSynchronize(s) || cudaGetLastError()) break;
-    st = 0;
-  } while (false);
-  cudaFree(work);
-  cudaFree(ctl);
-  red_free(&red);
-  return st;
+  // grow-only scratch reused across updates (an optimisation loop calls this every step)
+  static double *work = nullptr;
+  static int64_t work_n = 0;
+  static MmaCtl *ctl = nullptr;
+  static RedScratch red{};
+  if (!ctl && (dalloc(&ctl, 1) || red_alloc(&red))) return B200FEM_E_CUDA;
+  if (work_n < n) {
+    cudaStreamSynchronize(s);
+    cudaFree(work);
+    work = nullptr;
+    work_n = 0;
+    if (dalloc(&work, 4 * n)) return B200FEM_E_CUDA;
+    work_n = n;
+  }
+  MmaCtl h{};
+  h.g_value = g_value;
+  B200_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  MmaArgs a{x, dj, g_grad, lb, ub, x_prev, x_prev2, lower, upper, work, work + n, work + 2 * n, work + 3 * n,
+            x_new, asym_init, asym_expand, asym_shrink, move_limit, use_history};
+  const int gv = grid_n(n), gr = std::min(kRedBlocks, gv);
+  k_mma_absmax<<<gv, kThreads, 0, s>>>(n, dj, ctl);
+  k_mma_prep<<<gv, kThreads, 0, s>>>(n, a, ctl);
+  for (int e = 0; e < 1 + 41 + 100; ++e) k_mma_eval<false><<<gr, kThreads, 0, s>>>(n, a, ctl, red);
+  k_mma_eval<true><<<gv, kThreads, 0, s>>>(n, a, ctl, red);
+  count_launch(2 + 142 + 1);
+  B200_CUDA(cudaStreamSynchronize(s));  // h (the control block source) must outlive the copy
+  B200_CUDA(cudaGetLastError());
+  return 0;
 }
 
 }  // extern "C"

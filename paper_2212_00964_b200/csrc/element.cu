@@ -1215,6 +1215,7 @@ int b200fem_l2_field_error(int64_t n_cells, const double *coords, const int32_t 
   if (n_cells < 0 || !out_host) return B200FEM_E_INVALID;
   out_host[0] = out_host[1] = 0.0;
   if (n_cells == 0) return 0;
+  element_tables_init();
   cudaStream_t s = (cudaStream_t)stream;
   RedScratch red{};
   double *d = nullptr;

@@ -8,6 +8,8 @@ c4: J2 n^3, z=0 clamped, u_z = 0.012 ramp_and_back(10)            20 load steps 
 c5: SIMP-LE 176x88x22, theta ~ U(0.3, 0.9) seeds 0..9             one Newton solve per design (warm start)
 c5adj: the adjoint half of one config-5 design iteration: K assembly + K^T,
        adjoint BiCGSTAB on the compliance load, design VJP; plus the K^T kernel's GB/s
+c5topo: full topology-optimisation iterations on the config-5 mesh, per phase:
+        forward, compliance, adjoint, VJP, density filter (build once + apply), MMA update
 """
 
 import argparse
@@ -142,13 +144,51 @@ def c5adj():
     return out
 
 
+def c5topo(steps=3):
+    from paper_2212_00964_b200.adjoint import adjoint_solve, total_derivative
+    from paper_2212_00964_b200.inverse import (MmaState, compliance, compliance_load_vector, density_filter,
+                                               filter_sensitivities, mma_update)
+
+    mesh = fem.generate_box_mesh(176, 88, 22, 8.0, 4.0, 1.0)
+    x0 = fem.BoundaryLocator.plane(0, 0.0)
+    specs = [fem.DirichletSpec(x0, c, lambda p: 0.0) for c in range(3)]
+    neu = [fem.NeumannSpec(fem.boundary_facets(mesh, fem.BoundaryLocator.plane(0, 8.0)),
+                           lambda p: np.broadcast_to([0.0, 0.0, -1.0], np.asarray(p).shape[:-1] + (3,)))]
+    prob = fem.SimpElasticityProblem(mesh, fem.LinearElastic(ALU), specs, neu, penalty=3.0)
+    fem.workspace(prob)
+    lin = fem.LinearSolveConfig(method="pcg")
+    edge = 8.0 / 176
+    filt, t_fb, _ = timed(lambda: density_filter(mesh, 1.5 * edge))
+    n = mesh.n_cells
+    theta = D.to_device(np.full(n, 0.5))
+    st = MmaState.fresh(n)
+    c_grad = D.to_device(np.full(n, 1.0 / n))
+    f = D.to_device(compliance_load_vector(prob))
+    U = D.zeros(prob.n_dofs)
+    rows = []
+    for k in range(steps):
+        prob.set_theta(D.to_host(theta))
+        (U, rep), t_fw, _ = timed(lambda: fem.newton_solve(prob, U, lin_cfg=lin))
+        c, t_c, _ = timed(lambda: compliance(prob, U))
+        lam, t_adj, _ = timed(lambda: adjoint_solve(prob, U, f, lin_cfg=lin))
+        th = D.to_device(prob.theta)
+        sens, t_vjp, _ = timed(lambda: total_derivative(prob, U, lam, th))
+        sens, t_f, _ = timed(lambda: filter_sensitivities(filt, th, sens, prob.theta_min))
+        gv = float(theta.mean()) - 0.5
+        theta, t_mma, _ = timed(lambda: mma_update(st, theta, sens, gv, c_grad, prob.theta_min, 1.0))
+        rows.append({"compliance": c, "forward_s": t_fw, "compliance_s": t_c, "adjoint_s": t_adj, "vjp_s": t_vjp,
+                     "filter_s": t_f, "mma_s": t_mma, "pcg_iters": [s.iterations for s in rep.linear_stats]})
+    return {"config": "c5topo SIMP-LE 176x88x22 topology optimisation (pcg)", "n_cells": n, "filter_nnz": filt.nnz,
+            "filter_build_s": t_fb, "steps": rows}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="c1,c2,c4,c5")
     ap.add_argument("--c4n", type=int, default=40)
     a = ap.parse_args()
     runs = {"c1": lambda: [c1()], "c2": lambda: [c2()], "c4": lambda: [c4(a.c4n)],
-            "c5": lambda: [c5("bicgstab"), c5("pcg")], "c5adj": lambda: [c5adj()]}
+            "c5": lambda: [c5("bicgstab"), c5("pcg")], "c5adj": lambda: [c5adj()], "c5topo": lambda: [c5topo()]}
     for name in a.only.split(","):
         for r in runs[name]():
             print(json.dumps(r), flush=True)
