@@ -358,7 +358,7 @@ def run_ours(args):
                        if part is not None else "single GPU"),
         "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "k_spmv_fem3_tma (CSR SpMV, node-blocked columns, cp.async.bulk pipeline)", "bound": "hbm",
+        "roofline": {"kernel": "k_spmv_fem3_tma2 (CSR SpMV, node-blocked columns, cp.async.bulk pipeline, half-warp per node)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "bytes_per_launch": bytes_fem,
                      "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,

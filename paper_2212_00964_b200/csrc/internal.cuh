@@ -148,6 +148,7 @@ struct Matrix {
   int32_t *chunk_node = nullptr;
   int n_chunks = 0;
   bool use_tma = false;
+  int npw = 2;  // bulk-copy SpMV: nodes per consumer warp (2: half-warp per node; 1: warp per node)
   // rows computed by matvec/Krylov: node range (FEM3) or row range (CSR); -1 = all
   int64_t row_lo = 0, row_hi = -1;
   // Dirichlet identity rows (FEM matrices): PCG starts from x_d = b_d so that the Krylov

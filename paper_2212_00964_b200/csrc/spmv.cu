@@ -270,13 +270,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+constexpr uint32_t kMbarSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   uint32_t ok = 0;
-  do {
+  do {  // suspend-time hint: a waiting warp sleeps instead of re-polling (issue slots, power)
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(kMbarSuspendNs)
         : "memory");
   } while (!ok);
 }
@@ -475,6 +476,162 @@ static int tma_x_variant() {
   return v;
 }
 
+// Two nodes per consumer warp (half-warp per node, two neighbours per lane): the per-node
+// bookkeeping (chunk/pointer loads, address math, barrier waits) is shared by two nodes, so
+// the warp-instruction count per node roughly halves -- less SM energy per byte, which is
+// what limits the kernel once a long solve runs into the board power cap.  16 consumer warps
+// keep the same number of gathers in flight as 31 warps with one neighbour per lane.
+constexpr int kT2Consumers = 16;
+constexpr int kT2Threads = (kT2Consumers + 1) * 32;
+constexpr int kT2ExtBytes = 800;  // <= 96 rows + alignment slack
+constexpr int kT2StageBytes = kTmaValBytes + kTmaNbrBytes + 3 * kT2ExtBytes;
+constexpr int kT2Smem = kTmaStages * kT2StageBytes + 2 * kTmaStages * 8;
+
+// 16-lane reduce-scatter of three row partials: lanes 0, 4, 8 of each half-warp end with
+// rows 0, 1, 2 (full-warp shuffles; both halves reduce independently).
+__device__ __forceinline__ double half_sum3(double y0, double y1, double y2, int lane) {
+  const bool h8 = lane & 8;
+  const double s0 = h8 ? y0 : y2, s1 = h8 ? y1 : 0.0;
+  double k0 = (h8 ? y2 : y0) + __shfl_xor_sync(0xffffffffu, s0, 8);
+  double k1 = (h8 ? 0.0 : y1) + __shfl_xor_sync(0xffffffffu, s1, 8);
+  const bool h4 = lane & 4;
+  double kk = (h4 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h4 ? k0 : k1, 4);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+  return kk;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kT2Threads, 1) k_spmv_fem3_tma2(const int32_t *__restrict__ nbr_ptr,
+                                                                 const int32_t *__restrict__ nbr,
+                                                                 const double *__restrict__ data,
+                                                                 const int32_t *__restrict__ chunk_node, int n_chunks,
+                                                                 int64_t total_blocks, int64_t n_rows, SpmvArgs a,
+                                                                 RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kT2StageBytes);
+  uint64_t *empty = full + kTmaStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kT2Consumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t val_end = (uint64_t)total_blocks * 72, nbr_end = (uint64_t)total_blocks * 4;
+  const uint64_t row_end = (uint64_t)n_rows * 8;
+  double red0 = 0.0, red1 = 0.0;
+  if (warp == kT2Consumers) {
+    if (lane == 0) {  // producer
+      int it = 0;
+      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int s = it % kTmaStages;
+        const uint32_t ph = (it / kTmaStages) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        const int64_t cn0 = __ldg(chunk_node + c), cn1 = __ldg(chunk_node + c + 1);
+        const int64_t p0 = __ldg(nbr_ptr + cn0), p1 = __ldg(nbr_ptr + cn1);
+        const uint64_t vb0 = (72ull * p0) & ~15ull, vb1 = std::min((72ull * p1 + 15) & ~15ull, val_end & ~15ull);
+        const uint64_t nb0 = (4ull * p0) & ~15ull, nb1 = std::min((4ull * p1 + 15) & ~15ull, nbr_end & ~15ull);
+        const uint64_t eb0 = (24ull * cn0) & ~15ull, eb1 = std::min((24ull * cn1 + 15) & ~15ull, row_end & ~15ull);
+        const uint32_t ext_bytes = eb1 > eb0 ? (uint32_t)(eb1 - eb0) : 0u;
+        mbar_expect_tx(full + s, (uint32_t)((vb1 - vb0) + (nb1 - nb0)) + n_ext<MODE>() * ext_bytes);
+        uint8_t *stage = smem + s * kT2StageBytes;
+        if (vb1 > vb0) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(data) + vb0, (uint32_t)(vb1 - vb0), full + s);
+        if (nb1 > nb0)
+          bulk_g2s(stage + kTmaValBytes, reinterpret_cast<const uint8_t *>(nbr) + nb0, (uint32_t)(nb1 - nb0), full + s);
+#pragma unroll
+        for (int k = 0; k < n_ext<MODE>(); ++k)
+          if (ext_bytes)
+            bulk_g2s(stage + kTmaValBytes + kTmaNbrBytes + k * kT2ExtBytes,
+                     reinterpret_cast<const uint8_t *>(ext_ptr<MODE>(a, k)) + eb0, ext_bytes, full + s);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int hl = lane & 15;
+    const bool row_lane = (hl & 3) == 0 && hl < 12;
+    int it = 0;
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+      const int s = it % kTmaStages;
+      const uint32_t ph = (it / kTmaStages) & 1;
+      const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
+      const int64_t pc = __ldg(nbr_ptr + n0), pe = __ldg(nbr_ptr + n1);
+      const uint64_t vb0 = (72ull * pc) & ~15ull, nb0 = (4ull * pc) & ~15ull;
+      const bool tail = (72ull * pe > (val_end & ~15ull)) || (4ull * pe > (nbr_end & ~15ull)) ||
+                        (n_ext<MODE>() > 0 && 24ull * n1 > (row_end & ~15ull));
+      const uint64_t eb0 = (24ull * n0) & ~15ull;
+      const uint8_t *stage = smem + s * kT2StageBytes;
+      const int nA = n0 + 2 * warp + (lane >> 4);
+      const bool has = nA < n1;
+      int64_t pA = 0;
+      int cA = 0;
+      if (has) {
+        pA = __ldg(nbr_ptr + nA);
+        cA = __ldg(nbr_ptr + nA + 1) - (int)pA;
+      }
+      const int64_t row = 3 * (int64_t)nA + (hl >> 2);
+      RowPre pre{0.0, 0.0, 0.0, 0.0};
+      if (tail && row_lane && has) pre = spmv_preload<MODE>(row, a);
+      mbar_wait(full + s, ph);
+      if (!tail && row_lane && has && n_ext<MODE>() > 0) {
+        const uint8_t *ext = stage + kTmaValBytes + kTmaNbrBytes + (8ull * row - eb0);
+        pre = row_pre_from<MODE>(reinterpret_cast<const double *>(ext),
+                                 reinterpret_cast<const double *>(ext + kT2ExtBytes),
+                                 reinterpret_cast<const double *>(ext + 2 * kT2ExtBytes));
+      }
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      if (has) {
+        const double *sv = tail ? data + 9 * pA : reinterpret_cast<const double *>(stage + (72ull * pA - vb0));
+        const int32_t *sn = tail ? nbr + pA : reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0));
+        const int L = 3 * cA;
+        for (int j = hl; j < cA; j += 32) {  // both neighbours' gathers in flight together
+          const int j2 = j + 16;
+          const bool two = j2 < cA;
+          double x0, x1, x2, z0 = 0.0, z1 = 0.0, z2 = 0.0;
+          load_x3<0>(a.x, sn[j], x0, x1, x2);
+          if (two) load_x3<0>(a.x, sn[j2], z0, z1, z2);
+          const double *r0 = sv + 3 * j;
+          y0 = fma(r0[2], x2, fma(r0[1], x1, fma(r0[0], x0, y0)));
+          y1 = fma(r0[L + 2], x2, fma(r0[L + 1], x1, fma(r0[L], x0, y1)));
+          y2 = fma(r0[2 * L + 2], x2, fma(r0[2 * L + 1], x1, fma(r0[2 * L], x0, y2)));
+          if (two) {
+            const double *r1 = sv + 3 * j2;
+            y0 = fma(r1[2], z2, fma(r1[1], z1, fma(r1[0], z0, y0)));
+            y1 = fma(r1[L + 2], z2, fma(r1[L + 1], z1, fma(r1[L], z0, y1)));
+            y2 = fma(r1[2 * L + 2], z2, fma(r1[2 * L + 1], z1, fma(r1[2 * L], z0, y2)));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      const double acc = half_sum3(y0, y1, y2, lane);
+      if (has && row_lane) spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+    }
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kT2Consumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
+      spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
+static void set_t2_attr() {
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+  cudaFuncSetAttribute(k_spmv_fem3_tma2<SP_CGRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem);
+}
+
+static int tma_npw_env() {  // B200FEM_SPMV_NPW=1 selects the warp-per-node kernel (read per matrix)
+  const char *e = getenv("B200FEM_SPMV_NPW");
+  return (e && !strcmp(e, "1")) ? 1 : 2;
+}
+
 // Pack consecutive nodes into chunks whose values + neighbour ids fit one stage
 // (with 16-byte alignment slack), at most one node per consumer warp.
 int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
@@ -486,11 +643,13 @@ int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
   cudaFree(m->chunk_node);
   m->chunk_node = nullptr;
   m->use_tma = false;
+  m->npw = tma_npw_env();
   std::vector<int32_t> ch{(int32_t)lo};
   int64_t start = lo;
   for (int64_t n = lo; n < hi; ++n) {
     const int64_t nb = ptr[n + 1] - ptr[start];
-    const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= kTmaConsumers;
+    const int max_nodes = m->npw == 2 ? 2 * kT2Consumers : kTmaConsumers;
+    const bool fits = 72 * nb + 32 <= kTmaValBytes && 4 * nb + 32 <= kTmaNbrBytes && (n + 1 - start) <= max_nodes;
     if (!fits) {
       if (n == start) return 0;  // a single node does not fit a stage: keep the LDG kernel
       ch.push_back((int32_t)n);
@@ -507,6 +666,7 @@ int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
     set_tma_attr<0>();
     set_tma_attr<1>();
     set_tma_attr<2>();
+    set_t2_attr();
     attr = true;
   }
   m->use_tma = true;
@@ -741,6 +901,12 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = std::min(sms, m->n_chunks);
+    if (m->npw == 2) {
+      k_spmv_fem3_tma2<MODE><<<g, kT2Threads, kT2Smem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
+                                                                    m->n_chunks, m->nnz / 9, m->n, a, r);
+      count_launch();
+      return;
+    }
     switch (tma_x_variant()) {
       case 1: k_spmv_fem3_tma<MODE, 1><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
                                                                                 m->n_chunks, m->nnz / 9, m->n, a, r); break;
