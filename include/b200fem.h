@@ -150,6 +150,16 @@ int b200fem_ctx_sym_size(const b200fem_ctx *ctx, int64_t *n_values);
 int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U_dev, double *data_dev /* nullable */,
                          double *sym_dev, b200fem_error *err);
 int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double *sym_dev);
+/* GRID3: the same operator for contexts whose connectivity is a z-major box lattice
+ * (generate_box_mesh, mesh.py:134-168): self + 13 upper-offset node blocks stored as 14
+ * offset-major arrays (pre-Dirichlet), lower blocks read back as their transposes, identity
+ * Dirichlet rows.  grid_size gives 0 values when the mesh is not a lattice (dims = nodes per
+ * axis, nullable).  Replaces the K passed to bicgstab_jacobi by newton_solve
+ * (solvers.py:177-184, 218) -- assemble_jacobian still returns the reference CSR. */
+int b200fem_ctx_grid_size(const b200fem_ctx *ctx, int64_t *n_values, int32_t *dims /* [3], nullable */);
+int b200fem_jacobian_grid(b200fem_ctx *ctx, const double *U_dev, double *data_dev /* nullable */,
+                          double *grid_dev, b200fem_error *err);
+int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid_dev);
 /* generic CSR on the device (any square matrix with sorted unique columns) */
 int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr_dev,
                        const int32_t *indices_dev, const double *data_dev, void *stream);

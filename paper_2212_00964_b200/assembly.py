@@ -256,6 +256,28 @@ class DeviceWorkspace:
                                              D.ptr(sym), C.byref(err))
         raise_for(st, err, "jacobian_sym")
 
+    @property
+    def has_grid(self) -> bool:
+        """True when the connectivity is a z-major box lattice (GRID3 operator available)."""
+        return self.grid_size() > 0
+
+    def grid_size(self) -> int:
+        if self.vec != 3:
+            return 0
+        if not hasattr(self, "_grid_size"):
+            n = C.c_int64()
+            raise_for(_lib.lib().b200fem_ctx_grid_size(self.ctx, C.byref(n), None), None, "grid_size")
+            self._grid_size = n.value
+        return self._grid_size
+
+    def jacobian_grid(self, problem, U, grid, data=None):
+        """Self + upper-offset node blocks of the tangent in GRID3 layout (optionally also CSR)."""
+        self.sync(problem)
+        err = _lib.Error()
+        st = _lib.lib().b200fem_jacobian_grid(self.ctx, D.ptr(U), D.ptr(data) if data is not None else None,
+                                              D.ptr(grid), C.byref(err))
+        raise_for(st, err, "jacobian_grid")
+
     def param_vjp(self, problem, U, theta, w, out):
         """out <- w_eff^T dR/dtheta at (U, theta) on the device (assembly.py:303-341)."""
         err = _lib.Error()

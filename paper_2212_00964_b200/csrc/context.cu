@@ -299,6 +299,30 @@ static double host_detJ(const double *X /*8x3*/, int q) {
   return J[0][0] * A + J[0][1] * D + J[0][2] * G;
 }
 
+// GRID3 applies when the connectivity is exactly a z-major box lattice, i.e. the cells of
+// generate_box_mesh (mesh.py:152-167; also every z-slab part of one): cell i + nx j + nx ny k
+// has vertices base + {0, 1, NX+1, NX, NXY, NXY+1, NXY+NX+1, NXY+NX}, base = i + NX j + NXY k.
+static void detect_grid(Ctx *c, const int64_t *cells_h) {
+  if (c->vec != 3 || getenv("B200FEM_NO_GRID")) return;
+  const int64_t ne = c->n_cells, nn = c->n_nodes;
+  const int64_t NX = cells_h[3], NXY = cells_h[4];
+  if (NX < 2 || NXY < 2 * NX || NXY % NX || nn % NXY) return;
+  const int64_t NY = NXY / NX, NZ = nn / NXY;
+  const int64_t nx = NX - 1, ny = NY - 1, nz = NZ - 1;
+  if (nz < 1 || nx * ny * nz != ne) return;
+  const int64_t pat[8] = {0, 1, NX + 1, NX, NXY, NXY + 1, NXY + NX + 1, NXY + NX};
+  for (int64_t e = 0; e < ne; ++e) {
+    const int64_t i = e % nx, j = (e / nx) % ny, k = e / (nx * ny);
+    const int64_t base = i + NX * j + NXY * k;
+    for (int v = 0; v < 8; ++v)
+      if (cells_h[8 * e + v] != base + pat[v]) return;
+  }
+  c->grid_nx = (int)NX;
+  c->grid_ny = (int)NY;
+  c->grid_nz = (int)NZ;
+  c->grid_npad = (nn + 2) & ~1ll;  // even: every array starts 16-byte aligned; one block of slack
+}
+
 static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem_error *err) {
   cudaStream_t s = c->stream;
   const int64_t nn = c->n_nodes, ne = c->n_cells;
@@ -431,6 +455,8 @@ static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem
     cudaFree(ucnt);
     c->n_sym_blocks = nb;
   }
+
+  detect_grid(c, cells_h);
 
   // ---- colouring
   std::vector<int32_t> order;

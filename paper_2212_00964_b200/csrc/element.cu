@@ -776,7 +776,8 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
     const int32_t *__restrict__ n2c_ptr, const int32_t *__restrict__ n2c, const uint8_t *__restrict__ n2c_a,
     const uint8_t *__restrict__ cpos, const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr,
     const double *__restrict__ Ke, const uint8_t *__restrict__ dir_flag, int64_t n_nodes, int max_nbr,
-    double *__restrict__ data, const int32_t *__restrict__ up_ptr, double *__restrict__ sym) {
+    double *__restrict__ data, const int32_t *__restrict__ up_ptr, double *__restrict__ sym,
+    double *__restrict__ grid = nullptr, int gnx = 0, int gny = 0, int64_t gnpad = 0) {
   extern __shared__ double gsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double *acc = gsm + (size_t)w * VEC * VEC * max_nbr;
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
       __syncwarp();  // ascending cell order per slot
     }
     int self = 0;
-    if (dir_flag || sym) {
+    if (dir_flag || sym || grid) {
       int hi = cnt;  // position of n in its own neighbour list
       while (self < hi) {
         const int mid = (self + hi) >> 1;
@@ -823,6 +824,18 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
       for (int t = lane; t < nu * VEC * VEC; t += 32) {
         const int jb = t / (VEC * VEC), rr = t - jb * VEC * VEC, i = rr / VEC, kk = rr - i * VEC;
         o[t] = acc[i * L + VEC * (self + jb) + kk];
+      }
+      __syncwarp();
+    }
+    if (VEC == 3 && grid) {  // GRID3: upper blocks into the 126 element arrays (pre-Dirichlet)
+      const int gnxy = gnx * gny;
+      const int ni = (int)(n % gnx), nj = (int)((n / gnx) % gny), nk = (int)(n / gnxy);
+      const int nu = cnt - self;
+      for (int t = lane; t < nu * 9; t += 32) {
+        const int jb = t / 9, rr = t - jb * 9, i = rr / 3, kk = rr - i * 3;
+        const int m = __ldg(nbr + p0 + self + jb);
+        const int kx = grid_index(m % gnx - ni, (m / gnx) % gny - nj, m / gnxy - nk);
+        grid[(9 * kx + rr) * gnpad + n] = acc[i * L + 3 * (self + jb) + kk];
       }
       __syncwarp();
     }
@@ -1111,7 +1124,7 @@ int launch_param_vjp(Ctx *c, const double *U, const double *theta, const double 
 
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
-int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym) {
+int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym, double *grid) {
   cudaStream_t s = c->stream;
   const int vv = c->vec * c->vec;
   if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
@@ -1131,7 +1144,8 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_jacobian_gather<3><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
                                                      c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
-                                                     c->max_nbr, data, c->up_ptr, sym);
+                                                     c->max_nbr, data, c->up_ptr, sym, grid, c->grid_nx,
+                                                     c->grid_ny, c->grid_npad);
   } else {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_jacobian_gather<1><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
@@ -1201,6 +1215,13 @@ int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U, double *data, double
   Ctx *c = (Ctx *)ctx;
   if (c->vec != 3 || !sym) return B200FEM_E_INVALID;
   return launch_jacobian(c, U, data, err, sym);
+}
+
+int b200fem_jacobian_grid(b200fem_ctx *ctx, const double *U, double *data, double *grid, b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  Ctx *c = (Ctx *)ctx;
+  if (!c || c->vec != 3 || !c->grid_nx || !grid) return B200FEM_E_INVALID;
+  return launch_jacobian(c, U, data, err, nullptr, grid);
 }
 
 int b200fem_param_vjp(b200fem_ctx *ctx, const double *U, const double *theta, const double *w, double *out,

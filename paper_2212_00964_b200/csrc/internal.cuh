@@ -97,6 +97,10 @@ struct Ctx {
   int32_t *up_ptr = nullptr;  // (n_nodes+1)
   int32_t *lo_blk = nullptr;  // (total neighbours) only lower entries used
   int64_t n_sym_blocks = 0;
+  // GRID3 (vec 3 box lattices, see spmv.cu): nodes per axis (0 = not a lattice) and the
+  // padded length of each of the 14 offset arrays of upper node blocks
+  int grid_nx = 0, grid_ny = 0, grid_nz = 0;
+  int64_t grid_npad = 0;
   int max_nbr = 0;
   int max_deg = 0;              // max cells per node
   int32_t *n2c_ptr = nullptr;   // (n_nodes+1) node -> incident cells, ascending cell id
@@ -133,7 +137,7 @@ struct KrylovWork {
   cudaEvent_t ev[2]{};
 };
 
-enum MatKind : int { MK_CSR = 0, MK_FEM3 = 1, MK_SYM3 = 2 };
+enum MatKind : int { MK_CSR = 0, MK_FEM3 = 1, MK_SYM3 = 2, MK_GRID3 = 3 };
 struct Matrix {
   MatKind kind = MK_CSR;
   int64_t n = 0, nnz = 0;
@@ -158,7 +162,31 @@ struct Matrix {
   // SYM3: upper node blocks (pre-Dirichlet) + Dirichlet row flags applied on output rows
   const int32_t *up_ptr = nullptr, *lo_blk = nullptr;
   const uint8_t *dir_flag = nullptr;
+  // GRID3: lattice nodes per axis and the padded offset-array length (data = 14 arrays)
+  int gnx = 0, gny = 0, gnz = 0;
+  int64_t gnpad = 0;
 };
+
+// ------------------------------------------------------------------ GRID3 offsets
+// The 14 lattice offsets (di, dj, dk) with (dk, dj, di) lexicographically >= 0: the self
+// block and the 13 "upper" neighbours of a node in a z-major box lattice (node id
+// i + NX j + NX NY k, mesh.py:152-158).  Offset k of node n stores the 3x3 block
+// K[(n, n + off_k)] in array k (row-major, pre-Dirichlet); the lower block of
+// (n, n - off_k) is the transpose of array k's block of node n - off_k.
+__host__ __device__ constexpr int grid_di(int k) {
+  return k == 0 ? 0 : k == 1 ? 1 : k <= 4 ? k - 3 : (k - 5) % 3 - 1;
+}
+__host__ __device__ constexpr int grid_dj(int k) { return k <= 1 ? 0 : k <= 4 ? 1 : (k - 5) / 3 - 1; }
+__host__ __device__ constexpr int grid_dk(int k) { return k <= 4 ? 0 : 1; }
+// index of lattice offset (di, dj, dk) among the 14, or -1 for a "lower" offset
+__host__ __device__ inline int grid_index(int di, int dj, int dk) {
+  if (dk == 1) return 5 + 3 * (dj + 1) + (di + 1);
+  if (dk != 0) return -1;
+  if (dj == 1) return 3 + di;
+  if (dj != 0) return -1;
+  return di == 0 ? 0 : di == 1 ? 1 : -1;
+}
+int prepare_grid3(Matrix *m);
 
 // allocation helpers
 template <class T>
@@ -196,7 +224,8 @@ int prepare_sym3_chunks(Matrix *m);
 // element kernels
 int launch_residual(Ctx *c, const double *U, double *R, double bc_scale, int apply_dirichlet,
                     b200fem_error *err, double *norm_host);
-int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym = nullptr);
+int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym = nullptr,
+                    double *grid = nullptr);
 int launch_qp_flux(Ctx *c, const double *U, double *out, b200fem_error *err);
 int launch_volume_average(Ctx *c, const double *U, double *out_host, b200fem_error *err);
 int launch_commit(Ctx *c, const double *U);

@@ -438,6 +438,42 @@ int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double 
   return 0;
 }
 
+int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid) {
+  Ctx *c = (Ctx *)ctx;
+  if (!out || !c || c->vec != 3 || !c->grid_nx || !grid) return B200FEM_E_INVALID;
+  Matrix *m = new Matrix();
+  m->kind = MK_GRID3;
+  m->n = c->n_dofs;
+  m->nnz = c->nnz;
+  m->data = grid;
+  m->stream = c->stream;
+  m->nbr_ptr = c->nbr_ptr;
+  m->nbr = c->nbr;
+  m->indptr = c->indptr;
+  m->dir_flag = c->n_dir ? c->dir_flag : nullptr;
+  m->dir_dofs = c->dir_dofs;
+  m->n_dir = c->n_dir;
+  m->gnx = c->grid_nx;
+  m->gny = c->grid_ny;
+  m->gnz = c->grid_nz;
+  m->gnpad = c->grid_npad;
+  int st = prepare_grid3(m);
+  if (st) {
+    delete m;
+    return st;
+  }
+  *out = (b200fem_matrix *)m;
+  return 0;
+}
+
+int b200fem_ctx_grid_size(const b200fem_ctx *ctx, int64_t *n_values, int32_t *dims) {
+  const Ctx *c = (const Ctx *)ctx;
+  if (!c || !n_values) return B200FEM_E_INVALID;
+  *n_values = c->grid_nx ? 14 * 9 * c->grid_npad : 0;
+  if (dims) dims[0] = c->grid_nx, dims[1] = c->grid_ny, dims[2] = c->grid_nz;
+  return 0;
+}
+
 int b200fem_ctx_sym_size(const b200fem_ctx *ctx, int64_t *n_values) {
   const Ctx *c = (const Ctx *)ctx;
   if (!c || c->vec != 3) return B200FEM_E_INVALID;

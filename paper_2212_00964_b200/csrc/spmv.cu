@@ -849,6 +849,123 @@ int prepare_sym3_chunks(Matrix *m) {
   return 0;
 }
 
+
+// ------------------------------------------------------------------------------------
+// GRID3: symmetric storage for z-major box lattices (generate_box_mesh, mesh.py:134-168).
+//
+// The tangent is symmetric outside the Dirichlet rows (which the reference replaces by
+// identity rows, assembly.py:297-299), and the node coupling of a lattice is the 27-point
+// stencil.  Only the self block and the 13 upper-offset blocks of every node are stored,
+// pre-Dirichlet, in 126 element arrays: value e (0..8, row-major) of the block
+// K[(n, n + off_k)] sits at grid[(9 k + e) npad + n] (offsets k = 0..13, internal.cuh).
+// Row block a is
+//     y_a = sum_k B_k[a] x_{a + off_k}  +  sum_{k >= 1} B_k[a - off_k]^T x_{a - off_k}
+// With a thread per node, every value load of a warp is one contiguous 256-byte segment,
+// for the upper blocks (index a) and for the lower ones alike (index a - off_k): no column
+// indices, no gather.  The lower values were streamed as upper values of node a - off_k at
+// most one lattice plane earlier (~19 MB at config 3) and are re-read from L2; the grid-stride
+// chunk order keeps all warps on one wavefront so they still are.
+// DRAM per matvec: 14*72 B per node + x + y = 2.72 GB at config 3 (FEM3 CSR: 5.33 GB).
+// Dirichlet rows give y = x (identity rows).  Summation order is fixed -> deterministic.
+constexpr int kGThreads = 256;
+constexpr int kGMinBlocks = 1;  // 255 registers: ILP per thread beats more warps (2/SM: +41 %)
+
+struct GridDims {
+  int nx, ny, nz, nxy, nn;  // nodes per axis, per plane, total
+  int64_t npad;             // element-array length
+};
+
+struct LatticePos {  // which faces of the lattice node a lies on
+  bool i0, iN, j0, jN, k0, kN;
+};
+// Lattice coordinates of node a = c0 + t from those of the chunk start (the divisions are
+// warp-uniform) plus a carry walk.
+__device__ __forceinline__ LatticePos lattice_pos(int a, int c0, const GridDims &g) {
+  int k = c0 / g.nxy, rem = c0 - k * g.nxy, j = rem / g.nx, i = rem - j * g.nx;
+  i += a - c0;
+  while (i >= g.nx) {
+    i -= g.nx;
+    if (++j == g.ny) j = 0, ++k;
+  }
+  return {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, k == 0, k == g.nz - 1};
+}
+// lattice neighbour (di, dj, dk) exists (compile-time offsets fold to predicate logic)
+__device__ __forceinline__ bool grid_has(const LatticePos &p, int di, int dj, int dk) {
+  return !((di < 0 && p.i0) || (di > 0 && p.iN) || (dj < 0 && p.j0) || (dj > 0 && p.jN) || (dk < 0 && p.k0) ||
+           (dk > 0 && p.kN));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const double *__restrict__ grid, GridDims g,
+                                                             const uint8_t *__restrict__ dir_flag, SpmvArgs a,
+                                                             RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  const int lane = threadIdx.x & 31;
+  const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int n_chunks = (g.nn + 31) >> 5;
+  const int64_t np = g.npad;
+  double red0 = 0.0, red1 = 0.0;
+  for (int c = warp0; c < n_chunks; c += nwarps) {
+    const int c0 = c << 5, node = c0 + lane;
+    if (node >= g.nn) continue;
+    const LatticePos p = lattice_pos(node, c0, g);
+    const double *__restrict__ x = a.x;
+    double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, di, dj, dk);
+      const int m = node + di + dj * g.nx + dk * g.nxy;
+      const double *B = grid + 9 * q * np + node;
+      double b[9], xm[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + e * np) : 0.0;  // first use: keep in L2
+#pragma unroll
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) yu[r] = fma(b[3 * r + 2], xm[2], fma(b[3 * r + 1], xm[1], fma(b[3 * r], xm[0], yu[r])));
+    }
+#pragma unroll
+    for (int q = 1; q < 14; ++q) {  // lower: B_q[a - off_q]^T x_{a - off_q}
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, -di, -dj, -dk);
+      const int m = node - di - dj * g.nx - dk * g.nxy;
+      const double *B = grid + 9 * q * np + m;
+      double b[9], xm[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldcs(B + e * np) : 0.0;  // last use: evict first
+#pragma unroll
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) yl[r] = fma(b[6 + r], xm[2], fma(b[3 + r], xm[1], fma(b[r], xm[0], yl[r])));
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t row = 3 * (int64_t)node + r;
+      const RowPre pre = spmv_preload<MODE>(row, a);
+      const double acc = (dir_flag && __ldg(dir_flag + row)) ? __ldg(x + row) : yu[r] + yl[r];
+      spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+    }
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kGThreads / 32>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
+      spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
+static GridDims grid_dims(const Matrix *m) {
+  GridDims g{};
+  g.nx = m->gnx, g.ny = m->gny, g.nz = m->gnz, g.nxy = m->gnx * m->gny, g.nn = (int)(m->n / 3), g.npad = m->gnpad;
+  return g;
+}
+
+int prepare_grid3(Matrix *m) {
+  m->n_chunks = (int)((m->n / 3 + 31) / 32);
+  return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
+}
+
 template <int MODE, int LANES>
 __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict__ indptr,
                                                        const int32_t *__restrict__ indices,
@@ -896,7 +1013,14 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
   RedScratch r = red ? *red : RedScratch{};
   const bool full = m->row_hi < 0;
-  if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
+  if (m->kind == MK_GRID3) {  // full range only (b200fem_matrix_fem_grid)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const GridDims g = grid_dims(m);
+    const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (m->n_chunks + 7) / 8));
+    k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, a, r);
+  } else if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -962,12 +1086,14 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
                                                        const int32_t *__restrict__ up_ptr,
                                                        const uint8_t *__restrict__ dflag,
                                                        const double *__restrict__ data, int64_t row_lo, int64_t n,
-                                                       double *diag, double *inv, RedScratch red) {
+                                                       double *diag, double *inv, RedScratch red, int64_t grid_npad) {
   double zeros[1] = {0.0};
   for (int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double d = 0.0;
-    if (up_ptr) {  // SYM3: entry (c,c) of the node's self block (first upper block)
+    if (grid_npad) {  // GRID3: entry (c,c) of the node's self block (k = 0, element 4c)
+      d = (dflag && dflag[i]) ? 1.0 : data[4 * (i % 3) * grid_npad + i / 3];
+    } else if (up_ptr) {  // SYM3: entry (c,c) of the node's self block (first upper block)
       d = (dflag && dflag[i]) ? 1.0 : data[9 * (int64_t)up_ptr[i / 3] + 4 * (i % 3)];
     } else if (slots) {
       d = data[slots[i]];
@@ -991,10 +1117,11 @@ int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red,
   const bool nodes = m->kind != MK_CSR;
   const int64_t lo = m->row_hi < 0 ? 0 : (nodes ? 3 * m->row_lo : m->row_lo);
   const int64_t hi = m->row_hi < 0 ? m->n : (nodes ? 3 * m->row_hi : m->row_hi);
-  const bool sym = m->kind == MK_SYM3;
+  const bool sym = m->kind == MK_SYM3 || m->kind == MK_GRID3;
   k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, sym ? nullptr : m->diag_slots,
-                                                     sym ? m->up_ptr : nullptr, sym ? m->dir_flag : nullptr, m->data,
-                                                     lo, hi, diag, inv, *red);
+                                                     m->kind == MK_SYM3 ? m->up_ptr : nullptr,
+                                                     sym ? m->dir_flag : nullptr, m->data, lo, hi, diag, inv, *red,
+                                                     m->kind == MK_GRID3 ? m->gnpad : 0);
   count_launch();
   if (n_zero) {
     double z = 0.0;

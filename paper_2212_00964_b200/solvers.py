@@ -20,7 +20,7 @@ from . import _lib
 from .assembly import assemble_jacobian, workspace
 from .errors import BreakdownError, LinearSolverError, NonConvergenceError, raise_for
 from .mesh import BoundaryLocator, locate_nodes
-from .sparse import CsrMatrix, SymOperator
+from .sparse import CsrMatrix, GridOperator, SymOperator
 
 __all__ = ["LinearSolveConfig", "NewtonConfig", "LoadSchedule", "LinearSolverError", "BreakdownError",
            "NonConvergenceError", "bicgstab_jacobi", "pcg_jacobi", "newton_solve", "incremental_solve", "reaction_force",
@@ -35,17 +35,21 @@ class LinearSolveConfig:
     # "bicgstab" = the reference solver (solvers.py:87-167, default); "pcg" = Jacobi-CG for
     # symmetric tangents (north_star "CG/BiCGSTAB", BASELINE config 2), same stopping rule
     method: str = "bicgstab"
-    # operator of the Newton-loop solves: "csr" = the assembled CSR values (default);
-    # "sym" = symmetric node-block storage for vec-3 problems (same operator, half the DRAM
-    # bytes, but L2-gather bound: 1.64 ms vs 0.85 ms per config-3 matvec, profiles/)
-    operator: str = "csr"
+    # operator of the Newton-loop solves (all the same linear operator as the assembled CSR):
+    #  "auto" (default) = "grid" when the mesh is a box lattice and vec = 3, else "csr";
+    #  "csr"  = the assembled reference CSR values;
+    #  "grid" = GRID3: self + 13 upper-offset node blocks, offset-major (half the DRAM bytes,
+    #           lower blocks re-read from L2 as contiguous slices; csrc/spmv.cu);
+    #  "sym"  = symmetric node-block storage for any vec-3 mesh (L2-gather bound: 1.64 ms vs
+    #           0.85 ms per config-3 matvec, profiles/)
+    operator: str = "auto"
 
     def __post_init__(self):
         if self.rel_tol <= 0 or self.abs_tol <= 0:
             raise ValueError("linear solver tolerances must be positive")
         if self.method not in ("bicgstab", "pcg"):
             raise ValueError(f"unknown linear solver {self.method!r}")
-        if self.operator not in ("sym", "csr"):
+        if self.operator not in ("auto", "grid", "sym", "csr"):
             raise ValueError(f"unknown operator {self.operator!r}")
 
 
@@ -150,6 +154,19 @@ class NewtonReport:
 def _tangent_matrix(problem, U, operator="csr"):
     """K at U; cached for jacobian_constant problems (solvers.py:177-184)."""
     ws = workspace(problem)
+    if operator in ("auto", "grid") and ws.has_grid:
+        if problem.jacobian_constant:
+            K = getattr(problem, "_jac_cache", None)
+            if isinstance(K, GridOperator):
+                return K
+        K = ws._cache.get("newton_grid")
+        if K is None:
+            K = GridOperator(ws)
+            ws._cache["newton_grid"] = K
+        ws.jacobian_grid(problem, U, K.device_data)
+        if problem.jacobian_constant:
+            problem._jac_cache = K
+        return K
     if operator == "sym" and ws.has_sym:
         key = "newton_sym"
         if problem.jacobian_constant:
@@ -166,7 +183,7 @@ def _tangent_matrix(problem, U, operator="csr"):
         return K
     if problem.jacobian_constant:
         K = getattr(problem, "_jac_cache", None)
-        if K is None:
+        if not isinstance(K, CsrMatrix):
             data = D.empty(ws.nnz)
             ws.jacobian(problem, U, data)
             K = CsrMatrix._from_workspace(ws, data)

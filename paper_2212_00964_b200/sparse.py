@@ -182,6 +182,61 @@ def _host(a, dtype):
     return np.ascontiguousarray(np.asarray(a), dtype=dtype)
 
 
+class _NodeBlockOperator:
+    """Base of the device-only tangent operators used inside the Newton loop."""
+
+    _ctor = None
+    _size = None
+
+    def __init__(self, ws):
+        self._ws = ws
+        self._n = ws.n_dofs
+        self.device_data = D.empty(getattr(ws, self._size)())
+        self._handle = None
+
+    @property
+    def shape(self):
+        return (self._n, self._n)
+
+    def _device_handle(self):
+        if self._handle is None:
+            h = C.c_void_p()
+            raise_for(getattr(_lib.lib(), self._ctor)(C.byref(h), self._ws.ctx, D.ptr(self.device_data)), None,
+                      self._ctor)
+            self._handle = h
+        return self._handle
+
+    def matvec(self, x):
+        as_host = not D.is_device_tensor(x)
+        xd = D.to_device(x)
+        y = D.empty(self._n)
+        raise_for(_lib.lib().b200fem_matvec(self._device_handle(), D.ptr(xd), D.ptr(y)), None, "matvec")
+        return D.to_host(y) if as_host else y
+
+    __matmul__ = matvec
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and _lib._lib is not None:
+            try:
+                _lib._lib.b200fem_matrix_destroy(h)
+            except Exception:
+                pass
+
+
+class GridOperator(_NodeBlockOperator):
+    """The tangent of a vec-3 box-lattice workspace in GRID3 storage (csrc/spmv.cu).
+
+    Same linear operator as the CSR Jacobian (identity Dirichlet rows).  Only the self block
+    and the 13 upper-offset 3x3 blocks of every node are stored, offset-major, so a matvec
+    streams 14*72 B per node instead of 27*72 B + column ids, and the lower blocks are
+    re-read as contiguous L2-resident slices.  Used by the Newton loop's Krylov solves;
+    ``assemble_jacobian`` still returns the reference CSR."""
+
+    _ctor = "b200fem_matrix_fem_grid"
+    _size = "grid_size"
+
+
 class SymOperator:
     """The tangent of a vec-3 workspace as a symmetric node-block operator (csrc SYM3).
 

@@ -40,7 +40,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--material", default="nh")
-    ap.add_argument("--operator", default="csr", choices=["csr", "sym"])
+    ap.add_argument("--operator", default="csr", choices=["csr", "sym", "grid"])
     a = ap.parse_args()
     prob = problem(a.n, a.material)
     ws = fem.workspace(prob)
@@ -51,6 +51,10 @@ def main():
         from paper_2212_00964_b200.sparse import SymOperator
         K = SymOperator(ws)
         ws.jacobian_sym(prob, U, K.device_data)
+    if a.operator == "grid":
+        from paper_2212_00964_b200.sparse import GridOperator
+        K = GridOperator(ws)
+        ws.jacobian_grid(prob, U, K.device_data)
     x = D.to_device(np.random.default_rng(0).standard_normal(N))
     y = D.empty(N)
     lib = _lib.lib()
@@ -91,6 +95,8 @@ def main():
     for _ in range(3):
         if a.operator == "sym":
             ws.jacobian_sym(prob, U, K.device_data)
+        elif a.operator == "grid":
+            ws.jacobian_grid(prob, U, K.device_data)
         else:
             ws.jacobian(prob, U, K.device_data)
     e1.record()
@@ -105,6 +111,8 @@ def main():
     if a.operator == "sym":  # DRAM bytes of the symmetric storage: upper blocks + lower block ids
         nsym = ws.sym_size()
         b_fem = 8 * nsym + 4 * (nnz // 9 - nsym // 9) + 4 * (nnz // 9) + 4 * (nn + 1) * 2 + 16 * N
+    if a.operator == "grid":  # DRAM bytes of GRID3: 14 blocks per node + x + y (+ 1 B/row flags)
+        b_fem = 14 * 72 * nn + 16 * N + N
     print(json.dumps({"n": a.n, "material": a.material, "operator": a.operator, "nnz": nnz, "spmv_us": t * 1e6,
                       "spmv_gbs_fem": b_fem / t / 1e9, "spmv_gbs_csr12": b_csr / t / 1e9,
                       "bicgstab_ms_per_iter": t_it * 1e3, "jacobian_ms": t_jac * 1e3,
