@@ -320,7 +320,7 @@ static void detect_grid(Ctx *c, const int64_t *cells_h) {
   c->grid_nx = (int)NX;
   c->grid_ny = (int)NY;
   c->grid_nz = (int)NZ;
-  c->grid_npad = (nn + 2) & ~1ll;  // even: every array starts 16-byte aligned; one block of slack
+  c->grid_npad = (nn + 31) & ~31ll;  // whole 32-node tiles (internal.cuh grid_idx)
 }
 
 static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem_error *err) {

@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
       }
       __syncwarp();
     }
-    if (VEC == 3 && grid) {  // GRID3: upper blocks into the 126 element arrays (pre-Dirichlet)
+    if (VEC == 3 && grid) {  // GRID3: upper blocks in the tiled element layout (pre-Dirichlet)
       const int gnxy = gnx * gny;
       const int ni = (int)(n % gnx), nj = (int)((n / gnx) % gny), nk = (int)(n / gnxy);
       const int nu = cnt - self;
@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
         const int jb = t / 9, rr = t - jb * 9, i = rr / 3, kk = rr - i * 3;
         const int m = __ldg(nbr + p0 + self + jb);
         const int kx = grid_index(m % gnx - ni, (m / gnx) % gny - nj, m / gnxy - nk);
-        grid[(9 * kx + rr) * gnpad + n] = acc[i * L + 3 * (self + jb) + kk];
+        grid[grid_idx(kx, rr, n, gnpad)] = acc[i * L + 3 * (self + jb) + kk];
       }
       __syncwarp();
     }

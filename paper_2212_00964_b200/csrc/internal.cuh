@@ -186,6 +186,12 @@ __host__ __device__ inline int grid_index(int di, int dj, int dk) {
   if (dj != 0) return -1;
   return di == 0 ? 0 : di == 1 ? 1 : -1;
 }
+// GRID3 value layout (tiled by 32 nodes): value e (0..8, row-major) of the block at offset k
+// of node n.  npad = 32 * ceil(n_nodes / 32).  A warp's 32 consecutive nodes read one
+// contiguous 256-byte segment per (k, e), and a thread's 9 values sit at +256 B strides.
+__host__ __device__ inline int64_t grid_idx(int k, int e, int64_t n, int64_t npad) {
+  return ((int64_t)k * (npad >> 5) + (n >> 5)) * 288 + e * 32 + (n & 31);
+}
 int prepare_grid3(Matrix *m);
 
 // allocation helpers

@@ -856,8 +856,8 @@ int prepare_sym3_chunks(Matrix *m) {
 // The tangent is symmetric outside the Dirichlet rows (which the reference replaces by
 // identity rows, assembly.py:297-299), and the node coupling of a lattice is the 27-point
 // stencil.  Only the self block and the 13 upper-offset blocks of every node are stored,
-// pre-Dirichlet, in 126 element arrays: value e (0..8, row-major) of the block
-// K[(n, n + off_k)] sits at grid[(9 k + e) npad + n] (offsets k = 0..13, internal.cuh).
+// pre-Dirichlet, as 126 element streams tiled by 32 nodes: value e (0..8, row-major) of the
+// block K[(n, n + off_k)] sits at grid[grid_idx(k, e, n)] (offsets k = 0..13, internal.cuh).
 // Row block a is
 //     y_a = sum_k B_k[a] x_{a + off_k}  +  sum_{k >= 1} B_k[a - off_k]^T x_{a - off_k}
 // With a thread per node, every value load of a warp is one contiguous 256-byte segment,
@@ -906,6 +906,7 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
   const int n_chunks = (g.nn + 31) >> 5;
   const int64_t np = g.npad;
   double red0 = 0.0, red1 = 0.0;
+  const int nch = (int)(np >> 5);
   for (int c = warp0; c < n_chunks; c += nwarps) {
     const int c0 = c << 5, node = c0 + lane;
     if (node >= g.nn) continue;
@@ -917,10 +918,10 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, di, dj, dk);
       const int m = node + di + dj * g.nx + dk * g.nxy;
-      const double *B = grid + 9 * q * np + node;
+      const double *B = grid + ((int64_t)(q * nch + c) * 288 + lane);
       double b[9], xm[3];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + e * np) : 0.0;  // first use: keep in L2
+      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // first use: normal L2 policy
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
@@ -931,10 +932,10 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, -di, -dj, -dk);
       const int m = node - di - dj * g.nx - dk * g.nxy;
-      const double *B = grid + 9 * q * np + m;
+      const double *B = grid + ((int64_t)(q * nch + (m >> 5)) * 288 + (m & 31));
       double b[9], xm[3];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldcs(B + e * np) : 0.0;  // last use: evict first
+      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldcs(B + 32 * e) : 0.0;  // last use: evict first
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
@@ -1092,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
        i += (int64_t)gridDim.x * blockDim.x) {
     double d = 0.0;
     if (grid_npad) {  // GRID3: entry (c,c) of the node's self block (k = 0, element 4c)
-      d = (dflag && dflag[i]) ? 1.0 : data[4 * (i % 3) * grid_npad + i / 3];
+      d = (dflag && dflag[i]) ? 1.0 : data[grid_idx(0, 4 * (i % 3), i / 3, grid_npad)];
     } else if (up_ptr) {  // SYM3: entry (c,c) of the node's self block (first upper block)
       d = (dflag && dflag[i]) ? 1.0 : data[9 * (int64_t)up_ptr[i / 3] + 4 * (i % 3)];
     } else if (slots) {
