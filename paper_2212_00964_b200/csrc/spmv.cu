@@ -897,19 +897,19 @@ __device__ __forceinline__ bool grid_has(const LatticePos &p, int di, int dj, in
 
 template <int MODE>
 __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const double *__restrict__ grid, GridDims g,
-                                                             const uint8_t *__restrict__ dir_flag, SpmvArgs a,
-                                                             RedScratch red) {
+                                                             const uint8_t *__restrict__ dir_flag, int node_lo,
+                                                             int node_hi, SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
   const int lane = threadIdx.x & 31;
   const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const int n_chunks = (g.nn + 31) >> 5;
+  const int c_lo = node_lo >> 5, n_chunks = (node_hi + 31) >> 5;  // rows of nodes [node_lo, node_hi)
   const int64_t np = g.npad;
   double red0 = 0.0, red1 = 0.0;
   const int nch = (int)(np >> 5);
-  for (int c = warp0; c < n_chunks; c += nwarps) {
+  for (int c = c_lo + warp0; c < n_chunks; c += nwarps) {
     const int c0 = c << 5, node = c0 + lane;
-    if (node >= g.nn) continue;
+    if (node < node_lo || node >= node_hi) continue;
     const LatticePos p = lattice_pos(node, c0, g);
     const double *__restrict__ x = a.x;
     double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
@@ -1014,13 +1014,15 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
   RedScratch r = red ? *red : RedScratch{};
   const bool full = m->row_hi < 0;
-  if (m->kind == MK_GRID3) {  // full range only (b200fem_matrix_fem_grid)
+  if (m->kind == MK_GRID3) {  // all nodes, or the owned node range of a partition
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const GridDims g = grid_dims(m);
-    const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (m->n_chunks + 7) / 8));
-    k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, a, r);
+    const int lo = full ? 0 : (int)m->row_lo, hi = full ? g.nn : (int)m->row_hi;  // node range
+    const int nch = ((hi + 31) >> 5) - (lo >> 5);
+    const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (nch + 7) / 8));
+    k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
   } else if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

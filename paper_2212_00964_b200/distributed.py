@@ -36,7 +36,7 @@ from .errors import NonConvergenceError, raise_for
 from .materials import QuadPointState
 from .mesh import FacetSet, Mesh
 from .solvers import LinearSolveConfig, NewtonConfig, NewtonReport, SolveStats
-from .sparse import CsrMatrix
+from .sparse import CsrMatrix, GridOperator
 
 
 # ------------------------------------------------------------------------------ plan
@@ -166,13 +166,15 @@ class Communicator:
 
 # ---------------------------------------------------------------------- solver
 class _Part:
-    def __init__(self, problem, plan: PartPlan):
+    def __init__(self, problem, plan: PartPlan, operator="auto"):
         self.plan = plan
         self.problem = subproblem(problem, plan)
         self.ws = workspace(self.problem)
         n = self.problem.n_dofs
         self.vec = self.problem.vec
-        self.K = CsrMatrix._from_workspace(self.ws, D.empty(self.ws.nnz))
+        # a plane-cut part of a box lattice is itself a lattice: same GRID3 operator as 1 GPU
+        self.grid = operator in ("auto", "grid") and self.ws.has_grid
+        self.K = GridOperator(self.ws) if self.grid else CsrMatrix._from_workspace(self.ws, D.empty(self.ws.nnz))
         h = self.K._device_handle()
         lib = _lib.lib()
         peers = np.array(plan.peers, dtype=np.int32)
@@ -191,6 +193,12 @@ class _Part:
         self.dU = D.empty(n)
         self.own_dofs = (lo * self.vec, hi * self.vec)
 
+    def assemble_tangent(self):
+        if self.grid:
+            self.ws.jacobian_grid(self.problem, self.U, self.K.device_data)
+        else:
+            self.ws.jacobian(self.problem, self.U, self.K.device_data)
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and _lib._lib is not None:
@@ -203,7 +211,7 @@ class PartitionedSolver:
     nccl mode: call from every rank of an initialised torch.distributed NCCL group; this
     process solves part `rank` of `world_size`.  local mode: `nparts` parts in this process."""
 
-    def __init__(self, problem, nparts=None, mode="auto", ranges=None, plane_cut=True):
+    def __init__(self, problem, nparts=None, mode="auto", ranges=None, plane_cut=True, operator="auto"):
         import torch.distributed as dist
 
         if mode == "auto":
@@ -222,7 +230,7 @@ class PartitionedSolver:
         self.comm = Communicator("nccl" if mode == "nccl" else "local", rank, world)
         ranks = [rank] if mode == "nccl" else list(range(nparts))
         self.plans = plan_parts(mesh, self.ranges, ranks)
-        self.parts = [_Part(problem, p) for p in self.plans]
+        self.parts = [_Part(problem, p, operator) for p in self.plans]
         self._ptrs = (C.c_void_p * len(self.parts))(*[p.handle.value for p in self.parts])
 
     @staticmethod
@@ -303,7 +311,7 @@ class PartitionedSolver:
                 return NewtonReport(norms, it, True, lin)
             for p in self.parts:
                 if not (p.problem.jacobian_constant and getattr(p, "_k_done", False)):
-                    p.ws.jacobian(p.problem, p.U, p.K.device_data)
+                    p.assemble_tangent()
                     p._k_done = True
                 lib.b200fem_scale(p.problem.n_dofs, -1.0, D.ptr(p.R), D.ptr(p.rhs), stream)
             lin.append(self.bicgstab(lin_cfg))

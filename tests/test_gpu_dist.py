@@ -76,3 +76,19 @@ def test_nccl_single_rank_communicator():
         assert rel(U2, U1) < 1e-9
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("operator", ["auto", "csr"])
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_partitioned_grid3_parts(operator, nparts):
+    """Plane-cut parts of a box lattice are lattices: they run the GRID3 operator over their
+    owned node range (operator="auto"), or the CSR one; both match the single-GPU solve."""
+    case = dict(CASES["nh_block"], dims=(7, 5, 12))
+    _, p1, _ = build("nh_block", case)
+    U1, r1 = fem.newton_solve(p1, **TIGHT)
+    _, p2, _ = build("nh_block", case)
+    s = PartitionedSolver(p2, nparts=nparts, mode="local", operator=operator)
+    assert all(p.grid == (operator == "auto") for p in s.parts)
+    rep = s.newton_solve(**TIGHT)
+    assert rep.n_iterations == r1.n_iterations
+    assert rel(s.gather_U(), U1) < 1e-9
