@@ -262,8 +262,6 @@ class DeviceWorkspace:
         return self.grid_size() > 0
 
     def grid_size(self) -> int:
-        if self.vec != 3:
-            return 0
         if not hasattr(self, "_grid_size"):
             n = C.c_int64()
             raise_for(_lib.lib().b200fem_ctx_grid_size(self.ctx, C.byref(n), None), None, "grid_size")

@@ -303,7 +303,7 @@ static double host_detJ(const double *X /*8x3*/, int q) {
 // generate_box_mesh (mesh.py:152-167; also every z-slab part of one): cell i + nx j + nx ny k
 // has vertices base + {0, 1, NX+1, NX, NXY, NXY+1, NXY+NX+1, NXY+NX}, base = i + NX j + NXY k.
 static void detect_grid(Ctx *c, const int64_t *cells_h) {
-  if (c->vec != 3 || getenv("B200FEM_NO_GRID")) return;
+  if (getenv("B200FEM_NO_GRID")) return;
   const int64_t ne = c->n_cells, nn = c->n_nodes;
   const int64_t NX = cells_h[3], NXY = cells_h[4];
   if (NX < 2 || NXY < 2 * NX || NXY % NX || nn % NXY) return;

@@ -827,15 +827,16 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
       }
       __syncwarp();
     }
-    if (VEC == 3 && grid) {  // GRID3: upper blocks in the tiled element layout (pre-Dirichlet)
+    if (grid) {  // GRID3: upper blocks in the tiled element layout (pre-Dirichlet)
       const int gnxy = gnx * gny;
       const int ni = (int)(n % gnx), nj = (int)((n / gnx) % gny), nk = (int)(n / gnxy);
       const int nu = cnt - self;
-      for (int t = lane; t < nu * 9; t += 32) {
-        const int jb = t / 9, rr = t - jb * 9, i = rr / 3, kk = rr - i * 3;
+      constexpr int VV = VEC * VEC;
+      for (int t = lane; t < nu * VV; t += 32) {
+        const int jb = t / VV, rr = t - jb * VV, i = rr / VEC, kk = rr - i * VEC;
         const int m = __ldg(nbr + p0 + self + jb);
         const int kx = grid_index(m % gnx - ni, (m / gnx) % gny - nj, m / gnxy - nk);
-        grid[grid_idx(kx, rr, n, gnpad)] = acc[i * L + 3 * (self + jb) + kk];
+        grid[grid_idx(kx, rr, n, gnpad, VV)] = acc[i * L + VEC * (self + jb) + kk];
       }
       __syncwarp();
     }
@@ -1150,7 +1151,8 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_jacobian_gather<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_jacobian_gather<1><<<gg, warps * 32, smem, s>>>(c->n2c_ptr, c->n2c, c->n2c_a, c->cpos, c->nbr_ptr, c->nbr,
                                                      c->scratch, c->n_dir ? c->dir_flag : nullptr, c->n_nodes,
-                                                     c->max_nbr, data, nullptr, nullptr);
+                                                     c->max_nbr, data, nullptr, nullptr, grid, c->grid_nx, c->grid_ny,
+                                                     c->grid_npad);
   }
   count_launch(2);
   B200_CUDA_E(cudaGetLastError(), err);
@@ -1220,7 +1222,7 @@ int b200fem_jacobian_sym(b200fem_ctx *ctx, const double *U, double *data, double
 int b200fem_jacobian_grid(b200fem_ctx *ctx, const double *U, double *data, double *grid, b200fem_error *err) {
   if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
   Ctx *c = (Ctx *)ctx;
-  if (!c || c->vec != 3 || !c->grid_nx || !grid) return B200FEM_E_INVALID;
+  if (!c || !c->grid_nx || !grid) return B200FEM_E_INVALID;
   return launch_jacobian(c, U, data, err, nullptr, grid);
 }
 

@@ -163,7 +163,7 @@ struct Matrix {
   const int32_t *up_ptr = nullptr, *lo_blk = nullptr;
   const uint8_t *dir_flag = nullptr;
   // GRID3: lattice nodes per axis and the padded offset-array length (data = 14 arrays)
-  int gnx = 0, gny = 0, gnz = 0;
+  int gnx = 0, gny = 0, gnz = 0, gvec = 3;
   int64_t gnpad = 0;
 };
 
@@ -189,8 +189,9 @@ __host__ __device__ inline int grid_index(int di, int dj, int dk) {
 // GRID3 value layout (tiled by 32 nodes): value e (0..8, row-major) of the block at offset k
 // of node n.  npad = 32 * ceil(n_nodes / 32).  A warp's 32 consecutive nodes read one
 // contiguous 256-byte segment per (k, e), and a thread's 9 values sit at +256 B strides.
-__host__ __device__ inline int64_t grid_idx(int k, int e, int64_t n, int64_t npad) {
-  return ((int64_t)k * (npad >> 5) + (n >> 5)) * 288 + e * 32 + (n & 31);
+// (vec 1: one value per block, vv = 1)
+__host__ __device__ inline int64_t grid_idx(int k, int e, int64_t n, int64_t npad, int vv = 9) {
+  return (((int64_t)k * (npad >> 5) + (n >> 5)) * vv + e) * 32 + (n & 31);
 }
 int prepare_grid3(Matrix *m);
 

@@ -440,9 +440,10 @@ int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double 
 
 int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid) {
   Ctx *c = (Ctx *)ctx;
-  if (!out || !c || c->vec != 3 || !c->grid_nx || !grid) return B200FEM_E_INVALID;
+  if (!out || !c || !c->grid_nx || !grid) return B200FEM_E_INVALID;
   Matrix *m = new Matrix();
   m->kind = MK_GRID3;
+  m->gvec = c->vec;
   m->n = c->n_dofs;
   m->nnz = c->nnz;
   m->data = grid;
@@ -469,7 +470,7 @@ int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double
 int b200fem_ctx_grid_size(const b200fem_ctx *ctx, int64_t *n_values, int32_t *dims) {
   const Ctx *c = (const Ctx *)ctx;
   if (!c || !n_values) return B200FEM_E_INVALID;
-  *n_values = c->grid_nx ? 14 * 9 * c->grid_npad : 0;
+  *n_values = c->grid_nx ? 14 * c->vec * c->vec * c->grid_npad : 0;
   if (dims) dims[0] = c->grid_nx, dims[1] = c->grid_ny, dims[2] = c->grid_nz;
   return 0;
 }

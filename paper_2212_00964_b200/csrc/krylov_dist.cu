@@ -378,7 +378,7 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
   if (!out || !m || own_node_lo < 0 || own_node_hi < own_node_lo) return B200FEM_E_INVALID;
   Part *P = new Part();
   P->m = m;
-  P->vec = m->kind == MK_CSR ? 1 : 3;
+  P->vec = m->kind == MK_CSR ? 1 : m->kind == MK_GRID3 ? m->gvec : 3;
   P->own_lo = own_node_lo;
   P->own_hi = own_node_hi;
   m->row_lo = own_node_lo;  // node range (FEM3/SYM3) == row range (vec-1 CSR)

@@ -956,14 +956,62 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
   }
 }
 
+// Scalar (vec 1, Poisson) GRID: one value per offset; a thread per node, 4 CTAs per SM.
+template <int MODE>
+__global__ void __launch_bounds__(kGThreads, 4) k_spmv_grid1(const double *__restrict__ grid, GridDims g,
+                                                             const uint8_t *__restrict__ dir_flag, int node_lo,
+                                                             int node_hi, SpmvArgs a, RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  const int lane = threadIdx.x & 31;
+  const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int c_lo = node_lo >> 5, n_chunks = (node_hi + 31) >> 5;
+  const int nch = (int)(g.npad >> 5);
+  double red0 = 0.0, red1 = 0.0;
+  for (int c = c_lo + warp0; c < n_chunks; c += nwarps) {
+    const int c0 = c << 5, node = c0 + lane;
+    if (node < node_lo || node >= node_hi) continue;
+    const LatticePos p = lattice_pos(node, c0, g);
+    const double *__restrict__ x = a.x;
+    double yu = 0.0, yl = 0.0;
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, di, dj, dk);
+      const int m = node + di + dj * g.nx + dk * g.nxy;
+      const double b = ok ? __ldg(grid + ((int64_t)(q * nch + c) * 32 + lane)) : 0.0;
+      const double xm = ok ? __ldg(x + m) : 0.0;
+      yu = fma(b, xm, yu);
+    }
+#pragma unroll
+    for (int q = 1; q < 14; ++q) {
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, -di, -dj, -dk);
+      const int m = node - di - dj * g.nx - dk * g.nxy;
+      const double b = ok ? __ldcs(grid + ((int64_t)(q * nch + (m >> 5)) * 32 + (m & 31))) : 0.0;
+      const double xm = ok ? __ldg(x + m) : 0.0;
+      yl = fma(b, xm, yl);
+    }
+    const int64_t row = node;
+    const RowPre pre = spmv_preload<MODE>(row, a);
+    const double acc = (dir_flag && __ldg(dir_flag + row)) ? __ldg(x + row) : yu + yl;
+    spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+  }
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kGThreads / 32>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
+      spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
 static GridDims grid_dims(const Matrix *m) {
   GridDims g{};
-  g.nx = m->gnx, g.ny = m->gny, g.nz = m->gnz, g.nxy = m->gnx * m->gny, g.nn = (int)(m->n / 3), g.npad = m->gnpad;
+  g.nx = m->gnx, g.ny = m->gny, g.nz = m->gnz, g.nxy = m->gnx * m->gny, g.nn = (int)(m->n / m->gvec), g.npad = m->gnpad;
   return g;
 }
 
 int prepare_grid3(Matrix *m) {
-  m->n_chunks = (int)((m->n / 3 + 31) / 32);
+  m->n_chunks = (int)((m->n / m->gvec + 31) / 32);
   return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
 }
 
@@ -1021,8 +1069,13 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
     const GridDims g = grid_dims(m);
     const int lo = full ? 0 : (int)m->row_lo, hi = full ? g.nn : (int)m->row_hi;  // node range
     const int nch = ((hi + 31) >> 5) - (lo >> 5);
-    const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (nch + 7) / 8));
-    k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
+    if (m->gvec == 1) {
+      const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, (nch + 7) / 8));
+      k_spmv_grid1<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
+    } else {
+      const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (nch + 7) / 8));
+      k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
+    }
   } else if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1089,13 +1142,15 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
                                                        const int32_t *__restrict__ up_ptr,
                                                        const uint8_t *__restrict__ dflag,
                                                        const double *__restrict__ data, int64_t row_lo, int64_t n,
-                                                       double *diag, double *inv, RedScratch red, int64_t grid_npad) {
+                                                       double *diag, double *inv, RedScratch red, int64_t grid_npad,
+                                                       int gvec) {
   double zeros[1] = {0.0};
   for (int64_t i = row_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double d = 0.0;
     if (grid_npad) {  // GRID3: entry (c,c) of the node's self block (k = 0, element 4c)
-      d = (dflag && dflag[i]) ? 1.0 : data[grid_idx(0, 4 * (i % 3), i / 3, grid_npad)];
+      d = (dflag && dflag[i]) ? 1.0
+          : gvec == 3 ? data[grid_idx(0, 4 * (i % 3), i / 3, grid_npad)] : data[grid_idx(0, 0, i, grid_npad, 1)];
     } else if (up_ptr) {  // SYM3: entry (c,c) of the node's self block (first upper block)
       d = (dflag && dflag[i]) ? 1.0 : data[9 * (int64_t)up_ptr[i / 3] + 4 * (i % 3)];
     } else if (slots) {
@@ -1117,14 +1172,14 @@ __global__ void __launch_bounds__(kThreads) k_diagonal(const int32_t *__restrict
 }
 
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero) {
-  const bool nodes = m->kind != MK_CSR;
-  const int64_t lo = m->row_hi < 0 ? 0 : (nodes ? 3 * m->row_lo : m->row_lo);
-  const int64_t hi = m->row_hi < 0 ? m->n : (nodes ? 3 * m->row_hi : m->row_hi);
+  const int rpn = m->kind == MK_CSR ? 1 : m->kind == MK_GRID3 ? m->gvec : 3;  // rows per range unit
+  const int64_t lo = m->row_hi < 0 ? 0 : rpn * m->row_lo;
+  const int64_t hi = m->row_hi < 0 ? m->n : rpn * m->row_hi;
   const bool sym = m->kind == MK_SYM3 || m->kind == MK_GRID3;
   k_diagonal<<<kRedBlocks, kThreads, 0, m->stream>>>(m->indptr, m->indices, sym ? nullptr : m->diag_slots,
                                                      m->kind == MK_SYM3 ? m->up_ptr : nullptr,
                                                      sym ? m->dir_flag : nullptr, m->data, lo, hi, diag, inv, *red,
-                                                     m->kind == MK_GRID3 ? m->gnpad : 0);
+                                                     m->kind == MK_GRID3 ? m->gnpad : 0, m->gvec);
   count_launch();
   if (n_zero) {
     double z = 0.0;

@@ -225,12 +225,12 @@ class _NodeBlockOperator:
 
 
 class GridOperator(_NodeBlockOperator):
-    """The tangent of a vec-3 box-lattice workspace in GRID3 storage (csrc/spmv.cu).
+    """The tangent of a box-lattice workspace in GRID storage (csrc/spmv.cu GRID3).
 
     Same linear operator as the CSR Jacobian (identity Dirichlet rows).  Only the self block
-    and the 13 upper-offset 3x3 blocks of every node are stored, offset-major, so a matvec
-    streams 14*72 B per node instead of 27*72 B + column ids, and the lower blocks are
-    re-read as contiguous L2-resident slices.  Used by the Newton loop's Krylov solves;
+    and the 13 upper-offset node blocks (3x3 for vec 3, scalars for vec 1) are stored, tiled
+    element streams, so a vec-3 matvec streams 14*72 B per node instead of 27*72 B + column
+    ids, and the lower blocks are re-read from L2.  Used by the Newton loop's Krylov solves;
     ``assemble_jacobian`` still returns the reference CSR."""
 
     _ctor = "b200fem_matrix_fem_grid"

@@ -14,6 +14,7 @@ from pkg_cases import build
 pytestmark = pytest.mark.gpu
 
 VEC3 = ["c1", "nh_block", "j2_block", "simp", "simp_nh", "le_body", "nh_crit6"]
+VEC1 = ["poisson", "poisson_design"]
 # shapes that exercise the staged (bulk-copy) chunks, chunk tails, NX = 2 (offset aliasing
 # in linear ids) and long/flat lattices
 SHAPES = [(12, 7, 9), (1, 4, 30), (5, 1, 40), (31, 2, 6), (40, 3, 3), (6, 6, 6)]
@@ -37,7 +38,7 @@ def grid_of(prob, U):
     return G
 
 
-@pytest.mark.parametrize("name", VEC3)
+@pytest.mark.parametrize("name", VEC3 + VEC1)
 def test_grid_operator_equals_csr_jacobian(name, rng):
     g = load_golden(name)
     _, prob, U = build(name)
@@ -111,3 +112,30 @@ def test_grid_solve_deterministic():
         U, _ = fem.newton_solve(p, lin_cfg=fem.LinearSolveConfig(operator="grid"))
         outs.append(U)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_grid_scalar_operator_shapes(dims, rng):
+    """vec 1 (Poisson) GRID: one value per lattice offset."""
+    _, prob, U = build("poisson", dict(CASES["poisson"], dims=dims))
+    K = fem.assemble_jacobian(prob, U)
+    G = grid_of(prob, U)
+    x = rng.standard_normal(prob.n_dofs)
+    y = G @ x
+    assert rel(y, K @ x) < 1e-14
+    dd = fem.workspace(prob).dir_dofs
+    assert np.array_equal(y[dd], x[dd])
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "pcg"])
+def test_newton_grid_scalar_matches_csr(method):
+    case = dict(CASES["poisson"], dims=(11, 9, 13))
+    _, p1, _ = build("poisson", case)
+    _, p2, _ = build("poisson", case)
+    kw = dict(cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11))
+    U1, r1 = fem.newton_solve(p1, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method,
+                                                               operator="csr"), **kw)
+    U2, r2 = fem.newton_solve(p2, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method), **kw)
+    from paper_2212_00964_b200.sparse import GridOperator
+    assert isinstance(p2._jac_cache, GridOperator)
+    assert r1.n_iterations == r2.n_iterations and rel(U2, U1) < 1e-9

@@ -111,8 +111,8 @@ def main():
     if a.operator == "sym":  # DRAM bytes of the symmetric storage: upper blocks + lower block ids
         nsym = ws.sym_size()
         b_fem = 8 * nsym + 4 * (nnz // 9 - nsym // 9) + 4 * (nnz // 9) + 4 * (nn + 1) * 2 + 16 * N
-    if a.operator == "grid":  # DRAM bytes of GRID3: 14 blocks per node + x + y (+ 1 B/row flags)
-        b_fem = 14 * 72 * nn + 16 * N + N
+    if a.operator == "grid":  # GRID values: 14 blocks of vec^2 values per node + x + y (+ 1 B/row flags)
+        b_fem = 14 * 8 * vec * vec * nn + 16 * N + N
     print(json.dumps({"n": a.n, "material": a.material, "operator": a.operator, "nnz": nnz, "spmv_us": t * 1e6,
                       "spmv_gbs_fem": b_fem / t / 1e9, "spmv_gbs_csr12": b_csr / t / 1e9,
                       "bicgstab_ms_per_iter": t_it * 1e3, "jacobian_ms": t_jac * 1e3,
