@@ -80,3 +80,22 @@ def face_quadrature(mesh: Mesh, facets: np.ndarray) -> FaceQuadrature:
     tan = np.einsum("qag,fad->fqdg", dv, corners)
     area = np.linalg.norm(np.cross(tan[..., 0], tan[..., 1]), axis=-1)
     return FaceQuadrature(points=pts, JxW=area, shape_values=vals, local_nodes=local)
+
+
+def check_positive_jacobians(mesh: Mesh) -> None:
+    """Raise InvertedElementError if any cell is inverted (elements.py:115-131, 152-154):
+    det J by the cofactor expansion at the 8 Gauss points, first offender in (cell, qp)
+    order, the reference's message."""
+    qp = _tables()[0]
+    t = 1.0 + qp[:, None, :] * VERTEX_SIGNS
+    dN = np.stack([VERTEX_SIGNS[:, 0] * t[..., 1] * t[..., 2], VERTEX_SIGNS[:, 1] * t[..., 0] * t[..., 2],
+                   VERTEX_SIGNS[:, 2] * t[..., 0] * t[..., 1]], axis=-1) / 8.0
+    J = np.einsum("nka,qkb->nqab", mesh.cell_coords(), dN)
+    c0 = J[..., 1, 1] * J[..., 2, 2] - J[..., 1, 2] * J[..., 2, 1]
+    c1 = J[..., 1, 2] * J[..., 2, 0] - J[..., 1, 0] * J[..., 2, 2]
+    c2 = J[..., 1, 0] * J[..., 2, 1] - J[..., 1, 1] * J[..., 2, 0]
+    det = J[..., 0, 0] * c0 + J[..., 0, 1] * c1 + J[..., 0, 2] * c2
+    if np.any(det <= 0.0):
+        n, q = np.argwhere(det <= 0.0)[0]
+        raise InvertedElementError(f"non-positive Jacobian determinant {det[n, q]:.3e} "
+                                   f"(cell {n} of batch, quad point {q})")
