@@ -243,6 +243,15 @@ int b200fem_gather_sum(const double *x_dev, const int64_t *idx_dev, int64_t n, d
 int b200fem_axpy(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
 int b200fem_scale(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
 
+/* ---- host output formatting.  Rows of a (rows, cols) array as text lines,
+ * values space-separated, "%.17g" for doubles (= Python f"{x:.17g}", the reference's
+ * io_vtk._fmt, io_vtk.py:18-19), "%lld" for integers with an optional leading `prefix`
+ * column (the VTK CELLS count; < 0 = none).  Multi-threaded on the host.  Returns the bytes
+ * written, or -(bytes needed) when `out` is null or `cap` is too small. */
+int64_t b200fem_format_f64_rows(const double *v_host, int64_t rows, int32_t cols, char *out, int64_t cap);
+int64_t b200fem_format_i64_rows(const int64_t *v_host, int64_t rows, int32_t cols, int64_t prefix, char *out,
+                                int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,8 @@ SIGNATURES = {
     "b200fem_mma_update": (C.c_int, [_i64, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                      C.c_double, C.c_double, C.c_double, C.c_double, _vp, _vp]),
     "b200fem_l2_field_error": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _pf64, _vp]),
+    "b200fem_format_f64_rows": (C.c_int64, [_vp, _i64, C.c_int32, _vp, _i64]),
+    "b200fem_format_i64_rows": (C.c_int64, [_vp, _i64, C.c_int32, _i64, _vp, _i64]),
     "b200fem_gather_sum": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_axpy": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
     "b200fem_scale": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
@@ -149,6 +151,19 @@ def lib():
                         "no CUDA device: the forward-solve path runs only on the GPU (no CPU fallback)")
                 _lib = load_library()
     return _lib
+
+
+_host = None
+
+
+def host_lib():
+    """The library for its host-only entry points (output formatting): no device needed."""
+    global _host
+    if _host is None:
+        with _lock:
+            if _host is None:
+                _host = _lib if _lib is not None else load_library()
+    return _host
 
 
 def launch_count() -> int:
