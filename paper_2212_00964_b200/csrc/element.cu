@@ -788,6 +788,17 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
     const int L = VEC * cnt, T = VEC * L;
     for (int t = lane; t < T; t += 32) acc[t] = 0.0;
     __syncwarp();
+    int self = 0;
+    if (dir_flag || sym || grid) {
+      int hi = cnt;  // position of n in its own neighbour list
+      while (self < hi) {
+        const int mid = (self + hi) >> 1;
+        if (__ldg(nbr + p0 + mid) < (int)n) self = mid + 1; else hi = mid;
+      }
+    }
+    // GRID-only assembly (the Newton operator): only the upper blocks (neighbour >= n) are
+    // stored, so the lower half of the gather -- half the scratch reads -- is skipped.
+    const int min_pos = (grid && !sym && !data) ? self : 0;
     const int k0 = __ldg(n2c_ptr + n), deg = __ldg(n2c_ptr + n + 1) - k0;
     constexpr int ITEMS = 8 * VEC * VEC, PER = (ITEMS + 31) / 32;
     for (int kc = 0; kc < deg; ++kc) {
@@ -798,25 +809,18 @@ __global__ void __launch_bounds__(kThreads) k_jacobian_gather(
 #pragma unroll
       for (int r = 0; r < PER; ++r) {  // the cell's loads are issued together
         const int it = lane + 32 * r;
-        const bool ok = it < ITEMS;
         const int b = it / (VEC * VEC), rr = it - b * VEC * VEC, i = rr / VEC, kk = rr - i * VEC;
+        const int cp = it < ITEMS ? __ldg(cpos + e * 64 + a * 8 + b) : -1;
+        const bool ok = it < ITEMS && cp >= min_pos;
         const int pa = a <= b ? a : b, pb = a <= b ? b : a;
         const int off = a <= b ? i * VEC + kk : kk * VEC + i;
         v[r] = ok ? __ldg(Ke + (e * 36 + c_pair_idx[pa][pb]) * (VEC * VEC) + off) : 0.0;
-        pos[r] = ok ? i * L + VEC * __ldg(cpos + e * 64 + a * 8 + b) + kk : -1;
+        pos[r] = ok ? i * L + VEC * cp + kk : -1;
       }
 #pragma unroll
       for (int r = 0; r < PER; ++r)
         if (pos[r] >= 0) acc[pos[r]] += v[r];
       __syncwarp();  // ascending cell order per slot
-    }
-    int self = 0;
-    if (dir_flag || sym || grid) {
-      int hi = cnt;  // position of n in its own neighbour list
-      while (self < hi) {
-        const int mid = (self + hi) >> 1;
-        if (__ldg(nbr + p0 + mid) < (int)n) self = mid + 1; else hi = mid;
-      }
     }
     if (sym) {  // upper node blocks (m >= n), pre-Dirichlet, 3x3 row-major: the SYM3 operator
       double *o = sym + (int64_t)VEC * VEC * __ldg(up_ptr + n);
