@@ -160,6 +160,10 @@ int b200fem_ctx_grid_size(const b200fem_ctx *ctx, int64_t *n_values, int32_t *di
 int b200fem_jacobian_grid(b200fem_ctx *ctx, const double *U_dev, double *data_dev /* nullable */,
                           double *grid_dev, b200fem_error *err);
 int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid_dev);
+/* flags: B200FEM_GRID_PRE_DIRICHLET = the pre-Dirichlet tangent K0 (no identity rows): the
+ * adjoint's lambda_d = b_d - (K^T x)_d with x_d = 0 (adjoint.py:25-31, PCG split) */
+#define B200FEM_GRID_PRE_DIRICHLET 1
+int b200fem_matrix_fem_grid_ex(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid_dev, int32_t flags);
 /* generic CSR on the device (any square matrix with sorted unique columns) */
 int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr_dev,
                        const int32_t *indices_dev, const double *data_dev, void *stream);

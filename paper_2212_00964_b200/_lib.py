@@ -87,6 +87,7 @@ SIGNATURES = {
     "b200fem_ctx_grid_size": (C.c_int, [_vp, _pi64, C.POINTER(C.c_int32)]),
     "b200fem_jacobian_grid": (C.c_int, [_vp, _vp, _vp, _vp, _perr]),
     "b200fem_matrix_fem_grid": (C.c_int, [C.POINTER(_vp), _vp, _vp]),
+    "b200fem_matrix_fem_grid_ex": (C.c_int, [C.POINTER(_vp), _vp, _vp, C.c_int32]),
     "b200fem_matrix_set_data": (C.c_int, [_vp, _vp]),
     "b200fem_matrix_destroy": (C.c_int, [_vp]),
     "b200fem_matvec": (C.c_int, [_vp, _vp, _vp]),

@@ -439,6 +439,10 @@ int b200fem_matrix_fem_sym(b200fem_matrix **out, b200fem_ctx *ctx, const double 
 }
 
 int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid) {
+  return b200fem_matrix_fem_grid_ex(out, ctx, grid, 0);
+}
+
+int b200fem_matrix_fem_grid_ex(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid, int32_t flags) {
   Ctx *c = (Ctx *)ctx;
   if (!out || !c || !c->grid_nx || !grid) return B200FEM_E_INVALID;
   Matrix *m = new Matrix();
@@ -451,9 +455,10 @@ int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double
   m->nbr_ptr = c->nbr_ptr;
   m->nbr = c->nbr;
   m->indptr = c->indptr;
-  m->dir_flag = c->n_dir ? c->dir_flag : nullptr;
-  m->dir_dofs = c->dir_dofs;
-  m->n_dir = c->n_dir;
+  const bool raw = flags & B200FEM_GRID_PRE_DIRICHLET;  // K0: no identity rows
+  m->dir_flag = (c->n_dir && !raw) ? c->dir_flag : nullptr;
+  m->dir_dofs = raw ? nullptr : c->dir_dofs;
+  m->n_dir = raw ? 0 : c->n_dir;
   m->gnx = c->grid_nx;
   m->gny = c->grid_ny;
   m->gnz = c->grid_nz;

@@ -236,6 +236,28 @@ class GridOperator(_NodeBlockOperator):
     _ctor = "b200fem_matrix_fem_grid"
     _size = "grid_size"
 
+    def matvec_pre_dirichlet(self, x):
+        """K0 x: the same values without the identity Dirichlet rows (device in, device out)."""
+        h = getattr(self, "_raw", None)
+        if h is None:
+            h = C.c_void_p()
+            raise_for(_lib.lib().b200fem_matrix_fem_grid_ex(C.byref(h), self._ws.ctx, D.ptr(self.device_data), 1),
+                      None, "matrix_fem_grid_ex")
+            self._raw = h
+        xd = D.to_device(x)
+        y = D.empty(self._n)
+        raise_for(_lib.lib().b200fem_matvec(h, D.ptr(xd), D.ptr(y)), None, "matvec")
+        return y
+
+    def __del__(self):
+        h = getattr(self, "_raw", None)
+        if h is not None and _lib._lib is not None:
+            try:
+                _lib._lib.b200fem_matrix_destroy(h)
+            except Exception:
+                pass
+        super().__del__()
+
 
 class SymOperator:
     """The tangent of a vec-3 workspace as a symmetric node-block operator (csrc SYM3).
