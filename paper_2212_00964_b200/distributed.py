@@ -51,6 +51,52 @@ def node_ranges(n_nodes: int, nparts: int, plane: int | None = None):
     return [(cuts[k], cuts[k + 1]) for k in range(nparts)]
 
 
+def rcb_order(coords: np.ndarray, nparts: int):
+    """Recursive coordinate bisection of the nodes into `nparts` spatially compact parts.
+
+    Returns (perm, ranges): perm[new] = old node id with part 0's nodes first (original
+    relative order kept inside a part), and the contiguous new-id range of every part.  Used
+    for meshes whose numbering is not a z-major lattice (e.g. Gmsh files),
+    where contiguous ranges of the original ids would be scattered node sets with halos
+    spanning the whole mesh."""
+    parts = []
+
+    def split(ids, k):
+        if k == 1:
+            parts.append(np.sort(ids))
+            return
+        x = coords[ids]
+        axis = int(np.argmax(x.max(axis=0) - x.min(axis=0)))
+        k1 = k // 2
+        order = ids[np.argsort(x[:, axis], kind="stable")]
+        cut = int(round(ids.size * k1 / k))
+        split(order[:cut], k1)
+        split(order[cut:], k - k1)
+
+    split(np.arange(coords.shape[0]), nparts)
+    sizes = np.array([p.size for p in parts])
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    return np.concatenate(parts), [(int(cuts[i]), int(cuts[i + 1])) for i in range(nparts)]
+
+
+def renumbered(problem, perm):
+    """The same problem with node n' = perm^-1 (the mesh nodes reordered, cells unchanged):
+    geometric Dirichlet/Neumann/body data are re-located by the workspace; nodal designs are
+    permuted."""
+    mesh = problem.mesh
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    p2 = copy.copy(problem)
+    p2.mesh = Mesh(nodes=mesh.nodes[perm], cells=inv[mesh.cells])
+    p2._ws = None
+    if hasattr(p2, "_jac_cache"):
+        delattr(p2, "_jac_cache")
+    if getattr(problem, "design_layout", None) == "node":
+        p2.theta = np.asarray(problem.theta)[perm]
+        p2._theta_version = 0
+    return p2
+
+
 @dataclass
 class PartPlan:
     rank: int
@@ -211,7 +257,8 @@ class PartitionedSolver:
     nccl mode: call from every rank of an initialised torch.distributed NCCL group; this
     process solves part `rank` of `world_size`.  local mode: `nparts` parts in this process."""
 
-    def __init__(self, problem, nparts=None, mode="auto", ranges=None, plane_cut=True, operator="auto"):
+    def __init__(self, problem, nparts=None, mode="auto", ranges=None, plane_cut=True, operator="auto",
+                 reorder="auto"):
         import torch.distributed as dist
 
         if mode == "auto":
@@ -224,6 +271,14 @@ class PartitionedSolver:
             rank, world = 0, 1
             nparts = nparts or 2
         plane = self._plane_size(mesh) if plane_cut else None
+        # a mesh that is not a z-major lattice is renumbered by coordinate bisection so that
+        # every part is a compact node set (its halo is an interface, not the whole mesh)
+        self.perm = None
+        if ranges is None and (reorder is True or (reorder == "auto" and plane is None and nparts > 1)):
+            self.perm, ranges = rcb_order(mesh.nodes, nparts)
+            self.orig_problem = problem
+            problem = renumbered(problem, self.perm)
+            mesh = problem.mesh
         self.ranges = ranges or node_ranges(mesh.n_nodes, nparts, plane)
         self.mode = mode
         self.problem = problem
@@ -257,8 +312,9 @@ class PartitionedSolver:
         return out.value
 
     def residual_norm(self, apply_dirichlet=True) -> float:
+        scale = (self.orig_problem if self.perm is not None else self.problem).bc_scale
         for p in self.parts:
-            p.problem.bc_scale = self.problem.bc_scale
+            p.problem.bc_scale = scale
             p.ws.residual(p.problem, p.U, p.R, apply_dirichlet)
         return float(np.sqrt(self.dot("R", "R")))
 
@@ -271,9 +327,15 @@ class PartitionedSolver:
         raise_for(st, err, "dist_bicgstab")
         return SolveStats(info.iterations, info.matvecs, info.restarts, info.residual, info.tol)
 
+    def _dof_perm(self):
+        vec = self.problem.vec
+        return (self.perm[:, None] * vec + np.arange(vec)).ravel()  # new dof -> old dof
+
     def set_U(self, U):
-        """Scatter a global U (host or device, length N) into the parts' local vectors."""
+        """Scatter a global U (host or device, length N, original numbering) into the parts."""
         Ug = D.to_device(U)
+        if self.perm is not None:
+            Ug = Ug[D.to_device(self._dof_perm(), D.torch().int64)]
         vec = self.problem.vec
         for p in self.parts:
             idx = (p.plan.local_nodes[:, None] * vec + np.arange(vec)).ravel()
@@ -291,6 +353,10 @@ class PartitionedSolver:
             t = D.to_device(U)
             self.comm.allreduce_(t)  # disjoint owned blocks -> the sum is the concatenation
             U = D.to_host(t)
+        if self.perm is not None:  # back to the original numbering
+            Uo = np.empty_like(U)
+            Uo[self._dof_perm()] = U
+            U = Uo
         return U
 
     def newton_solve(self, U0=None, cfg: NewtonConfig = NewtonConfig(),

@@ -118,3 +118,28 @@ def test_plan_ghost_layers_single_process():
             assert np.isin(ix[ip[n]:ip[n + 1]], p.local_nodes).all()
     # interior part talks to both neighbours, end parts to one
     assert [len(p.peers) for p in plans] == [1, 2, 1]
+
+
+def test_rcb_order_compact_parts_on_shuffled_mesh():
+    """Coordinate bisection (distributed.rcb_order) of a mesh with shuffled node ids: balanced
+    contiguous parts after renumbering, and halos that are interfaces (far fewer ghost nodes
+    than contiguous ranges of the shuffled ids)."""
+    from paper_2212_00964_b200.distributed import rcb_order
+    from paper_2212_00964_b200.mesh import Mesh
+
+    box = generate_box_mesh(12, 10, 8, 1.2, 1.0, 0.8)
+    perm0 = np.random.default_rng(1).permutation(box.n_nodes)
+    inv0 = np.argsort(perm0)
+    mesh = Mesh(nodes=box.nodes[perm0], cells=inv0[box.cells])
+    for nparts in (2, 3, 4, 8):
+        perm, ranges = rcb_order(mesh.nodes, nparts)
+        assert np.array_equal(np.sort(perm), np.arange(mesh.n_nodes))
+        sizes = [hi - lo for lo, hi in ranges]
+        assert max(sizes) - min(sizes) <= 1 + mesh.n_nodes // 50
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(perm.size)
+        m2 = Mesh(nodes=mesh.nodes[perm], cells=inv[mesh.cells])
+        ghosts_rcb = sum(p.local_nodes.size - (p.own[1] - p.own[0]) for p in plan_parts(m2, ranges))
+        ghosts_raw = sum(p.local_nodes.size - (p.own[1] - p.own[0])
+                         for p in plan_parts(mesh, node_ranges(mesh.n_nodes, nparts)))
+        assert ghosts_rcb < 0.25 * ghosts_raw
