@@ -540,14 +540,19 @@ __global__ void k_res_dirichlet(double *__restrict__ R, const double *__restrict
 constexpr int kJacWarps = 4;
 
 template <int MAT>
+#ifndef JAC_NP
+#define JAC_NP 9
+#endif
 struct JacSmem {
+  // node dimension padded to JAC_NP: phase 1 stores [q][part + 4t][d] from lane (q, part),
+  // whose row stride decides the shared-memory bank conflicts
   double X[8][3];
   double U[8][3];
-  double g[8][8][3];
-  double h[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][8][3];  // NH: H g; J2: c3 * s g
-  double w[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][8][3];  // NH: c3 h - c2 u; J2: s g
-  double z[(MAT == B200FEM_MAT_NH) ? 8 : 1][8][3];
-  double t[(MAT == B200FEM_MAT_NH) ? 8 : 1][8][3];
+  double g[8][JAC_NP][3];
+  double h[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][JAC_NP][3];  // NH: H g; J2: c3 * s g
+  double w[(MAT == B200FEM_MAT_NH || MAT == B200FEM_MAT_J2) ? 8 : 1][JAC_NP][3];  // NH: c3 h - c2 u; J2: s g
+  double z[(MAT == B200FEM_MAT_NH) ? 8 : 1][JAC_NP][3];
+  double t[(MAT == B200FEM_MAT_NH) ? 8 : 1][JAC_NP][3];
   double coef[8][3];  // c1, cl, cm
 };
 
@@ -555,6 +560,53 @@ __device__ __forceinline__ double quad_sum(double v) {  // sum over the 4 lanes 
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
   return v;
+}
+
+// Contribution of quadrature point qq to the VEC x VEC block of pair (a0, b), added to K.
+template <int MAT, int VEC>
+__device__ __forceinline__ void jac_pair_qp(const JacSmem<MAT> &S, int a0, int b, int qq, double (&K)[VEC][VEC]) {
+    const double ga[3] = {S.g[qq][a0][0], S.g[qq][a0][1], S.g[qq][a0][2]};
+    const double gb[3] = {S.g[qq][b][0], S.g[qq][b][1], S.g[qq][b][2]};
+    const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
+    const double d = S.coef[qq][0] * gg;
+    if (MAT == B200FEM_MAT_POISSON) {
+      K[0][0] += d;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) K[i][i] += d;
+      if (MAT == B200FEM_MAT_LE || MAT == B200FEM_MAT_J2) {
+        const double cl = S.coef[qq][1], cm = S.coef[qq][2];
+        double la[3], ma[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          la[i] = cl * ga[i];
+          ma[i] = cm * gb[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) K[i][k] = fma(la[i], gb[k], fma(ma[i], ga[k], K[i][k]));
+      }
+      if (MAT == B200FEM_MAT_J2) {
+        const double ya[3] = {S.w[qq][a0][0], S.w[qq][a0][1], S.w[qq][a0][2]};
+        const double cyb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) K[i][k] = fma(ya[i], cyb[k], K[i][k]);
+      }
+      if (MAT == B200FEM_MAT_NH) {
+        const double ha[3] = {S.h[qq][a0][0], S.h[qq][a0][1], S.h[qq][a0][2]};
+        const double hb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
+        const double wb[3] = {S.w[qq][b][0], S.w[qq][b][1], S.w[qq][b][2]};
+        const double za[3] = {S.z[qq][a0][0], S.z[qq][a0][1], S.z[qq][a0][2]};
+        const double tb[3] = {S.t[qq][b][0], S.t[qq][b][1], S.t[qq][b][2]};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) K[i][k] = fma(ha[i], wb[k], fma(za[i], hb[k], fma(tb[i], ha[k], K[i][k])));
+      }
+    }
 }
 
 template <int MAT>
@@ -706,64 +758,50 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
       }
     }
     __syncwarp();
-    // ---- phase 2: the 36 symmetric pairs a <= b
-    for (int p = lane; p < 36; p += 32) {
-      const int a0 = c_pair_a[p], b = c_pair_b[p];
+    // ---- phase 2: the 36 symmetric pairs a <= b.  Round 1: lane p = pair p over all 8
+    // points.  Round 2: the last 4 pairs split over 8 lanes each (lane = one point), summed
+    // by a fixed 3-level shuffle tree -- 1.125 rounds of work instead of 2 (a second round
+    // of only 4 busy lanes).
+    {
+      const int p = lane, a0 = c_pair_a[p], b = c_pair_b[p];
       double K[VEC][VEC];
 #pragma unroll
       for (int i = 0; i < VEC; ++i)
 #pragma unroll
         for (int k = 0; k < VEC; ++k) K[i][k] = 0.0;
 #pragma unroll 2
-      for (int qq = 0; qq < 8; ++qq) {
-        const double ga[3] = {S.g[qq][a0][0], S.g[qq][a0][1], S.g[qq][a0][2]};
-        const double gb[3] = {S.g[qq][b][0], S.g[qq][b][1], S.g[qq][b][2]};
-        const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
-        const double d = S.coef[qq][0] * gg;
-        if (MAT == B200FEM_MAT_POISSON) {
-          K[0][0] += d;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 3; ++i) K[i][i] += d;
-          if (MAT == B200FEM_MAT_LE || MAT == B200FEM_MAT_J2) {
-            const double cl = S.coef[qq][1], cm = S.coef[qq][2];
-            double la[3], ma[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-              la[i] = cl * ga[i];
-              ma[i] = cm * gb[i];
-            }
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int k = 0; k < 3; ++k) K[i][k] = fma(la[i], gb[k], fma(ma[i], ga[k], K[i][k]));
-          }
-          if (MAT == B200FEM_MAT_J2) {
-            const double ya[3] = {S.w[qq][a0][0], S.w[qq][a0][1], S.w[qq][a0][2]};
-            const double cyb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int k = 0; k < 3; ++k) K[i][k] = fma(ya[i], cyb[k], K[i][k]);
-          }
-          if (MAT == B200FEM_MAT_NH) {
-            const double ha[3] = {S.h[qq][a0][0], S.h[qq][a0][1], S.h[qq][a0][2]};
-            const double hb[3] = {S.h[qq][b][0], S.h[qq][b][1], S.h[qq][b][2]};
-            const double wb[3] = {S.w[qq][b][0], S.w[qq][b][1], S.w[qq][b][2]};
-            const double za[3] = {S.z[qq][a0][0], S.z[qq][a0][1], S.z[qq][a0][2]};
-            const double tb[3] = {S.t[qq][b][0], S.t[qq][b][1], S.t[qq][b][2]};
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-              for (int k = 0; k < 3; ++k) K[i][k] = fma(ha[i], wb[k], fma(za[i], hb[k], fma(tb[i], ha[k], K[i][k])));
-          }
-        }
-      }
+      for (int qq = 0; qq < 8; ++qq) jac_pair_qp<MAT, VEC>(S, a0, b, qq, K);
       double *out = Ke + (e * 36 + p) * (VEC * VEC);
 #pragma unroll
       for (int i = 0; i < VEC; ++i)
 #pragma unroll
         for (int k = 0; k < VEC; ++k) out[i * VEC + k] = K[i][k];
+    }
+    {
+      const int p = 32 + (lane >> 3), qq = lane & 7, a0 = c_pair_a[p], b = c_pair_b[p];
+      double K[VEC][VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) K[i][k] = 0.0;
+      jac_pair_qp<MAT, VEC>(S, a0, b, qq, K);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          double v = K[i][k];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          K[i][k] = v;
+        }
+      if (qq == 0) {
+        double *out = Ke + (e * 36 + p) * (VEC * VEC);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) out[i * VEC + k] = K[i][k];
+      }
     }
     __syncwarp();
   }
