@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=136)
     p.add_argument("--stretch", type=float, default=0.02)
-    p.add_argument("--cpu-sample-n", type=int, default=12)
+    p.add_argument("--cpu-sample-n", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--linear", default="bicgstab", choices=["bicgstab", "pcg"],
                    help="Krylov method of the timed Newton solve (reference default: bicgstab)")
