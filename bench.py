@@ -177,6 +177,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
+# FP64 (non-tensor) DFMA peak measured on the pool's B200 (tools/fp64_peak.cu ->
+# profiles/r01_fp64_peak.json): the roofline denominator of the FP64-bound assembly kernels.
+FP64_PEAK_TFLOPS = 34.23
+# Algorithmic FLOPs per cell of the NH kernels (FMA = 2), counted from the factored algorithm
+# (DESIGN.md section 3): tangent = 8 points x ~960 (geometry, grad u, F, H, per-node vectors)
+# + 36 pairs x 8 points x 63 (block update); residual = 8 points x ~770.
+NH_TANGENT_FLOPS_PER_CELL = 8 * 960 + 36 * 8 * 63
+NH_RESIDUAL_FLOPS_PER_CELL = 8 * 770
+
+
 def ncu_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as fh:
@@ -391,6 +401,14 @@ def run_ours(args):
                      "jacobian_layout": "grid3" if grid_op else "csr",
                      "jacobian_csr_ms": t_jac_csr * 1e3, "jacobian_csr_mcells_s": n_cells_l / t_jac_csr / 1e6,
                      "jacobian_csr_hbm_gbs": (8 * ws.nnz + 32 * n_cells_l + 24 * n_nodes_l + 8 * Nl) / t_jac_csr / 1e9,
+                     "fp64_roofline": {
+                         "bound": "fp64", "peak_tflops": FP64_PEAK_TFLOPS, "peak_kind": "measured (tools/fp64_peak.cu)",
+                         "residual_flops_per_cell": NH_RESIDUAL_FLOPS_PER_CELL,
+                         "residual_tflops": NH_RESIDUAL_FLOPS_PER_CELL * n_cells_l / t_res / 1e12,
+                         "residual_frac": NH_RESIDUAL_FLOPS_PER_CELL * n_cells_l / t_res / 1e12 / FP64_PEAK_TFLOPS,
+                         "tangent_flops_per_cell": NH_TANGENT_FLOPS_PER_CELL,
+                         "tangent_tflops": NH_TANGENT_FLOPS_PER_CELL * n_cells_l / t_jac_csr / 1e12,
+                         "tangent_frac": NH_TANGENT_FLOPS_PER_CELL * n_cells_l / t_jac_csr / 1e12 / FP64_PEAK_TFLOPS},
                      "per_rank": world > 1},
         "setup_s": setup_s,
         "clocks": ck,
