@@ -139,6 +139,78 @@ void free_work(KrylovWork *w) {
   delete w;
 }
 
+
+// ------------------------------------------------------------ device-side Krylov loop
+// The iterations run as a CUDA graph WHILE node: its body is one captured iteration plus a
+// one-thread kernel that keeps the loop going while the device-side status is RUNNING.
+// Convergence, breakdown and max_iters are decided by the scalar stages on the device, so
+// the host launches one graph per (re)start and waits once -- no polling batches, and no
+// no-op launches after convergence (the batched loop enqueues up to 64 extra iterations).
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const KrylovScalars *S) {
+  cudaGraphSetConditional(h, S->status == KS_RUNNING ? 1u : 0u);
+}
+
+static bool use_graph_loop() {
+  static int v = -1;
+  if (v < 0) v = getenv("B200FEM_NO_GRAPH") ? 0 : 1;
+  return v == 1;
+}
+
+// Build (once per solve start: x and b may differ between calls) and run the while-graph of
+// `enqueue` on the matrix's stream; returns 0 or a CUDA error.
+template <class F>
+static int run_loop_graph(Matrix *m, F &&enqueue, b200fem_error *err) {
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  // capture needs a non-default stream (the caller's may be the legacy stream): the body is
+  // captured on a private stream, the graph then runs on the matrix's stream
+  static thread_local cudaStream_t cs = nullptr;
+  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), err, "capture stream");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaSuccess;
+  const char *where = "";
+  do {
+    where = "cudaGraphCreate";
+    if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) break;
+    where = "cudaGraphConditionalHandleCreate";
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) break;
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    where = "cudaGraphAddNode(while)";
+    if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np)) != cudaSuccess) break;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    where = "cudaStreamBeginCaptureToGraph";
+    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+      break;
+    m->stream = cs;
+    enqueue();
+    k_loop_cond<<<1, 1, 0, cs>>>(h, w->sc);
+    m->stream = s;
+    cudaGraph_t cap = nullptr;
+    where = "cudaStreamEndCapture";
+    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) break;
+    where = "cudaGraphInstantiate";
+    if ((e = cudaGraphInstantiate(&ge, g, 0)) != cudaSuccess) break;
+    where = "cudaGraphLaunch";
+    if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) break;
+  } while (false);
+  m->stream = s;
+  if (ge) cudaGraphExecDestroy(ge);  // deferred until the launch completes
+  if (g) cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_err(err, B200FEM_E_CUDA, "Krylov while-graph: %s failed: %s", where, cudaGetErrorString(e));
+    return B200FEM_E_CUDA;
+  }
+  return 0;
+}
+
 static int grid_vec(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
 
 static void enqueue_iteration(Matrix *m, const double *b, double *x) {
@@ -224,25 +296,34 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     B200_CUDA_E(cudaMemsetAsync(w->p, 0, n * sizeof(double), s), err);
     k_begin<<<1, 1, 0, s>>>(w->sc);
     count_launch();
-    // ---- inner loop: batches of iterations, double-buffered status polling
-    int batch = 4;
+    // ---- inner loop: a device-side while-graph, or batches with double-buffered polling
     int cur = 0;
-    auto enqueue_batch = [&](int slot) -> int {
-      for (int i = 0; i < batch; ++i) enqueue_iteration(m, b, x);
-      B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
-      B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
-      return 0;
-    };
-    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
     KrylovScalars done{};
-    for (;;) {
-      batch = std::min(batch * 2, 32);
-      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
-      B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
-      if (H[1 + cur].status != KS_RUNNING) break;
-      cur ^= 1;
+    if (use_graph_loop()) {
+      const long long it0 = it;
+      if (int rc = run_loop_graph(m, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
+      B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+      B200_CUDA_E(cudaStreamSynchronize(s), err);
+      count_launch(5 * (H[1].it - it0) + 1);
+      cur = 1;  // the snapshot is in H[1 + (cur ^ 1)]
+    } else {
+      int batch = 4;
+      auto enqueue_batch = [&](int slot) -> int {
+        for (int i = 0; i < batch; ++i) enqueue_iteration(m, b, x);
+        B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+        B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
+        return 0;
+      };
+      if (enqueue_batch(cur)) return B200FEM_E_CUDA;
+      for (;;) {
+        batch = std::min(batch * 2, 32);
+        if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
+        B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
+        if (H[1 + cur].status != KS_RUNNING) break;
+        cur ^= 1;
+      }
+      B200_CUDA_E(cudaStreamSynchronize(s), err);  // drain the no-op batch
     }
-    B200_CUDA_E(cudaStreamSynchronize(s), err);  // drain the no-op batch
     done = H[1 + (cur ^ 1)];                     // latest snapshot (status is sticky)
     it = done.it;
     mv = done.mv;
@@ -339,22 +420,32 @@ int pcg(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, doubl
     }
     k_begin_cg<<<1, 1, 0, s>>>(w->sc);
     count_launch();
-    int batch = 4, cur = 0;
-    auto enqueue_batch = [&](int slot) -> int {
-      for (int i = 0; i < batch; ++i) enqueue_cg_iteration(m, x);
-      B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
-      B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
-      return 0;
-    };
-    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
-    for (;;) {
-      batch = std::min(batch * 2, 32);
-      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
-      B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
-      if (H[1 + cur].status != KS_RUNNING) break;
-      cur ^= 1;
+    int cur = 0;
+    if (use_graph_loop()) {
+      const long long it0 = it;
+      if (int rc = run_loop_graph(m, [&] { enqueue_cg_iteration(m, x); }, err)) return rc;
+      B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+      B200_CUDA_E(cudaStreamSynchronize(s), err);
+      count_launch(3 * (H[1].it - it0) + 1);
+      cur = 1;
+    } else {
+      int batch = 4;
+      auto enqueue_batch = [&](int slot) -> int {
+        for (int i = 0; i < batch; ++i) enqueue_cg_iteration(m, x);
+        B200_CUDA_E(cudaMemcpyAsync(&H[1 + slot], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
+        B200_CUDA_E(cudaEventRecord(w->ev[slot], s), err);
+        return 0;
+      };
+      if (enqueue_batch(cur)) return B200FEM_E_CUDA;
+      for (;;) {
+        batch = std::min(batch * 2, 32);
+        if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
+        B200_CUDA_E(cudaEventSynchronize(w->ev[cur]), err);
+        if (H[1 + cur].status != KS_RUNNING) break;
+        cur ^= 1;
+      }
+      B200_CUDA_E(cudaStreamSynchronize(s), err);
     }
-    B200_CUDA_E(cudaStreamSynchronize(s), err);
     const KrylovScalars done = H[1 + (cur ^ 1)];
     it = done.it;
     mv = done.mv;
