@@ -36,7 +36,20 @@ struct Part {
   std::vector<int64_t> soff, roff; // node offsets into the packed buffers (n_peers + 1)
   int32_t *send_nodes = nullptr, *recv_nodes = nullptr;
   double *sendbuf = nullptr, *recvbuf = nullptr;
+  // halo / interior overlap (GRID3 parts): rows of [int_lo, int_hi) touch no ghost node, so
+  // their SpMV runs on s2 while the halo is exchanged; the two boundary bands follow it
+  bool overlap = false;
+  int64_t int_lo = 0, int_hi = 0;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+  RedScratch red_in{}, red_lo{}, red_hi{};  // partial dot totals of the three launches
 };
+
+// total of the three partial dot groups, in a fixed order (deterministic)
+__global__ void k_sum3(const double *a, const double *b, const double *c, double *out, int nv) {
+  const int j = threadIdx.x;
+  if (j < nv) out[j] = (a[j] + b[j]) + c[j];
+}
 
 __global__ void k_pack(const double *__restrict__ v, const int32_t *__restrict__ nodes, int64_t n, int vec,
                        double *__restrict__ buf) {
@@ -141,6 +154,43 @@ struct Dist {
     return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
   }
 
+  // y = op(A) v over the owned rows of every part, partial dot totals left in red.result
+  // (inline_stage 0): halo of v first, or overlapped with the interior rows (GRID3 parts)
+  int spmv(SpmvMode mode, const std::vector<SpmvArgs> &a, double *const *vec, int nv) {
+    for (size_t p = 0; p < parts.size(); ++p) {
+      Part *P = parts[p];
+      if (!P->overlap) continue;
+      Matrix *m = P->m;
+      B200_CUDA(cudaEventRecord(P->ev_in, stream(p)));
+      B200_CUDA(cudaStreamWaitEvent(P->s2, P->ev_in, 0));
+      cudaStream_t ms = m->stream;
+      m->stream = P->s2;
+      m->row_lo = P->int_lo, m->row_hi = P->int_hi;
+      if (launch_spmv(m, mode, a[p], &P->red_in)) return B200FEM_E_CUDA;
+      m->stream = ms;
+      B200_CUDA(cudaEventRecord(P->ev_done, P->s2));
+    }
+    if (int st = halo(vec)) return st;
+    for (size_t p = 0; p < parts.size(); ++p) {
+      Part *P = parts[p];
+      Matrix *m = P->m;
+      KrylovWork *w = m->kw;
+      if (!P->overlap) {
+        if (launch_spmv(m, mode, a[p], &w->red)) return B200FEM_E_CUDA;
+        continue;
+      }
+      m->row_lo = P->own_lo, m->row_hi = P->int_lo;
+      if (launch_spmv(m, mode, a[p], &P->red_lo)) return B200FEM_E_CUDA;
+      m->row_lo = P->int_hi, m->row_hi = P->own_hi;
+      if (launch_spmv(m, mode, a[p], &P->red_hi)) return B200FEM_E_CUDA;
+      m->row_lo = P->own_lo, m->row_hi = P->own_hi;
+      B200_CUDA(cudaStreamWaitEvent(stream(p), P->ev_done, 0));
+      k_sum3<<<1, 32, 0, stream(p)>>>(P->red_in.result, P->red_lo.result, P->red_hi.result, w->red.result, nv);
+      count_launch();
+    }
+    return 0;
+  }
+
   void stage(int kind) {
     for (size_t p = 0; p < parts.size(); ++p) {
       KrylovWork *w = parts[p]->m->kw;
@@ -177,12 +227,13 @@ static void enqueue_dist_iteration(Dist &D, double *const *x) {
     pv[p] = w->p;
     sv[p] = w->s;
   }
-  D.halo(pv.data());
+  std::vector<SpmvArgs> a1(np), a2(np);
   for (size_t p = 0; p < np; ++p) {
     KrylovWork *w = D.parts[p]->m->kw;
-    SpmvArgs a{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
-    launch_spmv(D.parts[p]->m, SP_JACOBI_R0, a, &w->red);
+    a1[p] = SpmvArgs{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
+    a2[p] = SpmvArgs{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
   }
+  D.spmv(SP_JACOBI_R0, a1, pv.data(), 1);
   D.allreduce(1);
   D.stage(ST_R0);
   for (size_t p = 0; p < np; ++p) {
@@ -192,12 +243,7 @@ static void enqueue_dist_iteration(Dist &D, double *const *x) {
     k_update_s<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->s + lo, w->sc);
     count_launch();
   }
-  D.halo(sv.data());
-  for (size_t p = 0; p < np; ++p) {
-    KrylovWork *w = D.parts[p]->m->kw;
-    SpmvArgs a{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
-    launch_spmv(D.parts[p]->m, SP_JACOBI_TT, a, &w->red);
-  }
+  D.spmv(SP_JACOBI_TT, a2, sv.data(), 2);
   D.allreduce(2);
   D.stage(ST_TT);
   for (size_t p = 0; p < np; ++p) {
@@ -273,12 +319,12 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
     H.mv = mv;
     for (size_t p = 0; p < np; ++p)
       B200_CUDA_E(cudaMemcpyAsync(D.parts[p]->m->kw->sc, &H, sizeof(H), cudaMemcpyHostToDevice, D.stream(p)), err);
-    if (D.halo(x)) return B200FEM_E_CUDA;
+    std::vector<SpmvArgs> ar(np);
     for (size_t p = 0; p < np; ++p) {
       KrylovWork *w = D.parts[p]->m->kw;
-      SpmvArgs ar{x[p], w->r, w->inv, w->diag, b[p], w->r0, w->sc, 0};
-      if (launch_spmv(D.parts[p]->m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
+      ar[p] = SpmvArgs{x[p], w->r, w->inv, w->diag, b[p], w->r0, w->sc, 0};
     }
+    if (D.spmv(SP_RESIDUAL, ar, x, 2)) return B200FEM_E_CUDA;
     if (D.allreduce(2)) return B200FEM_E_CUDA;
     D.stage(ST_RES);
     ++restarts;
@@ -383,6 +429,21 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
   P->own_hi = own_node_hi;
   m->row_lo = own_node_lo;  // node range (FEM3/SYM3) == row range (vec-1 CSR)
   m->row_hi = own_node_hi;
+  if (m->kind == MK_GRID3 && m->gvec == 3 && !getenv("B200FEM_NO_OVERLAP")) {
+    const int64_t margin = (int64_t)m->gnx * m->gny + m->gnx + 1;  // largest lattice offset
+    P->int_lo = own_node_lo + margin;
+    P->int_hi = own_node_hi - margin;
+    if (P->int_hi > P->int_lo && n_peers > 0) {
+      if (cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming) != cudaSuccess || red_alloc(&P->red_in) ||
+          red_alloc(&P->red_lo) || red_alloc(&P->red_hi)) {
+        delete P;
+        return B200FEM_E_CUDA;
+      }
+      P->overlap = true;
+    }
+  }
   if (m->kind == MK_FEM3 && m->use_tma) {  // bulk-copy chunks over the owned nodes only
     if (prepare_fem3_chunks(m, own_node_lo, own_node_hi)) {
       delete P;
@@ -418,6 +479,15 @@ int b200fem_part_destroy(b200fem_part *pp) {
   cudaFree(P->recv_nodes);
   cudaFree(P->sendbuf);
   cudaFree(P->recvbuf);
+  if (P->overlap) {
+    cudaStreamSynchronize(P->s2);
+    cudaStreamDestroy(P->s2);
+    cudaEventDestroy(P->ev_in);
+    cudaEventDestroy(P->ev_done);
+    red_free(&P->red_in);
+    red_free(&P->red_lo);
+    red_free(&P->red_hi);
+  }
   if (P->m) {
     P->m->row_lo = 0, P->m->row_hi = -1;
     if (P->m->use_tma) prepare_fem3_chunks(P->m);

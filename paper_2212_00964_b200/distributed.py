@@ -206,8 +206,11 @@ class Communicator:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and _lib._lib is not None:
-            _lib._lib.b200fem_comm_destroy(h)
+        try:  # at interpreter exit the module globals may already be gone
+            if h is not None and _lib._lib is not None:
+                _lib._lib.b200fem_comm_destroy(h)
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------- solver
@@ -247,8 +250,11 @@ class _Part:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and _lib._lib is not None:
-            _lib._lib.b200fem_part_destroy(h)
+        try:  # at interpreter exit the module globals may already be gone
+            if h is not None and _lib._lib is not None:
+                _lib._lib.b200fem_part_destroy(h)
+        except Exception:
+            pass
 
 
 class PartitionedSolver:
