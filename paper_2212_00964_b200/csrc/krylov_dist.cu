@@ -350,14 +350,27 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
       k_begin<<<1, 1, 0, D.stream(p)>>>(w->sc);
       count_launch();
     }
-    int batch = 4;
-    for (;;) {
+    // batches of iterations with double-buffered status polling: the next batch is enqueued
+    // before the previous one is waited on, so the GPUs never idle on the host's launches
+    // (the collectives of a batch enqueued past convergence still run: batches stay <= 16)
+    KrylovWork *w0 = D.parts[0]->m->kw;
+    int batch = 4, cur = 0;
+    auto enqueue_batch = [&](int slot) -> int {
       for (int i = 0; i < batch; ++i) enqueue_dist_iteration(D, x);
-      B200_CUDA_E(cudaMemcpyAsync(poll, D.parts[0]->m->kw->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)), err);
-      B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
-      if (poll->status != KS_RUNNING) break;
-      batch = std::min(batch * 2, 32);
+      B200_CUDA(cudaMemcpyAsync(poll + 1 + slot, w0->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)));
+      B200_CUDA(cudaEventRecord(w0->ev[slot], D.stream(0)));
+      return 0;
+    };
+    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
+    for (;;) {
+      batch = std::min(batch * 2, 16);
+      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
+      B200_CUDA_E(cudaEventSynchronize(w0->ev[cur]), err);
+      if (poll[1 + cur].status != KS_RUNNING) break;
+      cur ^= 1;
     }
+    for (size_t p = 0; p < np; ++p) B200_CUDA_E(cudaStreamSynchronize(D.stream(p)), err);
+    *poll = poll[1 + (cur ^ 1)];  // latest snapshot (status is sticky)
     B200_CUDA_E(cudaGetLastError(), err);
     it = poll->it;
     mv = poll->mv;
