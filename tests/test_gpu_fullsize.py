@@ -65,3 +65,21 @@ def test_fullsize_newton_paths_agree(solutions):
     norms = r0.residual_norms
     assert norms[-1] <= 1e-10 * norms[0]
     assert norms[3] < norms[2] ** 1.5  # quadratic convergence at the end
+
+
+def test_config2_poisson_matches_reference_values():
+    """BASELINE config 2 at full size (100^3 cells, 1.03M DOF): the reference's BiCGSTAB run
+    gives max u = 5.622140e-02 after 200 matvecs."""
+    mesh = fem.generate_box_mesh(100, 100, 100, 1.0, 1.0, 1.0)
+    onb = fem.BoundaryLocator(lambda p: (np.abs(np.asarray(p) - 0.5) >= 0.5 - 1e-9).any(axis=-1))
+    out = {}
+    for method in ("bicgstab", "pcg"):
+        prob = fem.PoissonProblem(mesh, 1.0, [fem.DirichletSpec(onb, 0, lambda p: 0.0)],
+                                  source=lambda p: np.ones(np.asarray(p).shape[:-1] + (1,)))
+        U, rep = fem.newton_solve(prob, lin_cfg=fem.LinearSolveConfig(method=method))
+        out[method] = (U, rep)
+    U, rep = out["bicgstab"]
+    assert abs(U.max() - 5.622140e-02) <= 5e-9  # the reference's 7 significant digits
+    mv = sum(s.matvecs for s in rep.linear_stats)
+    assert 180 <= mv <= 220  # reference: 200 (round-off moves Krylov counts by a few %)
+    assert rel(out["pcg"][0], U) < 1e-8

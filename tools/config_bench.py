@@ -72,7 +72,7 @@ def c2():
         (U, rep), dev, _ = timed(lambda: fem.newton_solve(prob, D.zeros(prob.n_dofs), lin_cfg=lin))
         out[method] = {"newton_s": dev, "setup_s": setup, "linear_iterations": [s.iterations for s in rep.linear_stats],
                        "matvecs": sum(s.matvecs for s in rep.linear_stats), "max_u": float(U.max()),
-                       "norms": rep.residual_norms}
+                       "norms": rep.residual_norms, "phase_s": getattr(rep, "timings", None)}
     out["n_dofs"] = prob.n_dofs
     out["reference_max_u"] = "5.622140e-02 (SURVEY 8(d), reference BiCGSTAB, 200 matvecs)"
     return out
