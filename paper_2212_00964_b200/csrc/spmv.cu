@@ -864,7 +864,8 @@ int prepare_sym3_chunks(Matrix *m) {
 // for the upper blocks (index a) and for the lower ones alike (index a - off_k): no column
 // indices, no gather.  The lower values were streamed as upper values of node a - off_k at
 // most one lattice plane earlier (~19 MB at config 3) and are re-read from L2; the grid-stride
-// chunk order keeps all warps on one wavefront so they still are.
+// chunk order keeps all warps on one wavefront so they still are (ncu: 2.73 GB of DRAM reads
+// per launch against 2.66 GB algorithmic).
 // DRAM per matvec: 14*72 B per node + x + y = 2.72 GB at config 3 (FEM3 CSR: 5.33 GB).
 // Dirichlet rows give y = x (identity rows).  Summation order is fixed -> deterministic.
 constexpr int kGThreads = 256;
@@ -928,14 +929,18 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
       for (int r = 0; r < 3; ++r) yu[r] = fma(b[3 * r + 2], xm[2], fma(b[3 * r + 1], xm[1], fma(b[3 * r], xm[0], yu[r])));
     }
 #pragma unroll
-    for (int q = 1; q < 14; ++q) {  // lower: B_q[a - off_q]^T x_{a - off_q}
+    // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
+    // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
+    // read may come first; an evict-first line would then be dropped before that second use
+    // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
+    for (int q = 1; q < 14; ++q) {
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, -di, -dj, -dk);
       const int m = node - di - dj * g.nx - dk * g.nxy;
       const double *B = grid + ((int64_t)(q * nch + (m >> 5)) * 288 + (m & 31));
       double b[9], xm[3];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldcs(B + 32 * e) : 0.0;  // last use: evict first
+      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // normal policy (see below)
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
