@@ -993,7 +993,7 @@ __global__ void __launch_bounds__(kGThreads, 4) k_spmv_grid1(const double *__res
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, -di, -dj, -dk);
       const int m = node - di - dj * g.nx - dk * g.nxy;
-      const double b = ok ? __ldcs(grid + ((int64_t)(q * nch + (m >> 5)) * 32 + (m & 31))) : 0.0;
+      const double b = ok ? __ldg(grid + ((int64_t)(q * nch + (m >> 5)) * 32 + (m & 31))) : 0.0;
       const double xm = ok ? __ldg(x + m) : 0.0;
       yl = fma(b, xm, yl);
     }
