@@ -609,8 +609,25 @@ __device__ __forceinline__ void jac_pair_qp(const JacSmem<MAT> &S, int a0, int b
     }
 }
 
+// Scratch layouts of the 36 symmetric cell blocks: cell-major [cell][pair][VV] for the ordered
+// per-node gather of the CSR / SYM3 paths, or element-major [pair][VV][cell] for the lattice
+// pull of the GRID path (consecutive nodes read consecutive cells: coalesced).
+template <int VEC>
+__device__ __forceinline__ void jac_store(double *__restrict__ Ke, int64_t e, int64_t n_cells, int p, int soa,
+                                          const double (&K)[VEC][VEC]) {
+  constexpr int VV = VEC * VEC;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i)
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      if (soa) Ke[((int64_t)p * VV + i * VEC + k) * n_cells + e] = K[i][k];
+      else Ke[(e * 36 + p) * VV + i * VEC + k] = K[i][k];
+    }
+}
+
 template <int MAT>
-__global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int64_t n, double *__restrict__ Ke) {
+__global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int64_t n, double *__restrict__ Ke,
+                                                                 int soa) {
   constexpr int VEC = (MAT == B200FEM_MAT_POISSON) ? 1 : 3;
   __shared__ JacSmem<MAT> sm_all[kJacWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -771,11 +788,7 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
         for (int k = 0; k < VEC; ++k) K[i][k] = 0.0;
 #pragma unroll 2
       for (int qq = 0; qq < 8; ++qq) jac_pair_qp<MAT, VEC>(S, a0, b, qq, K);
-      double *out = Ke + (e * 36 + p) * (VEC * VEC);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i)
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) out[i * VEC + k] = K[i][k];
+      jac_store<VEC>(Ke, e, n, p, soa, K);
     }
     {
       const int p = 32 + (lane >> 3), qq = lane & 7, a0 = c_pair_a[p], b = c_pair_b[p];
@@ -795,13 +808,7 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           K[i][k] = v;
         }
-      if (qq == 0) {
-        double *out = Ke + (e * 36 + p) * (VEC * VEC);
-#pragma unroll
-        for (int i = 0; i < VEC; ++i)
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) out[i * VEC + k] = K[i][k];
-      }
+      if (qq == 0) jac_store<VEC>(Ke, e, n, p, soa, K);
     }
     __syncwarp();
   }
@@ -1167,6 +1174,66 @@ int launch_param_vjp(Ctx *c, const double *U, const double *theta, const double 
   return fetch_element_errors(c, err, false);  // synchronises the stream
 }
 
+// GRID path, lattice pull (box meshes only): thread per node; for every upper lattice offset k
+// the 1, 2, 4 or 8 cells shared by node n and n + off_k are known from the lattice, and the
+// block is summed from the element-major scratch in ascending cell id -- the same order (and
+// the same values) as the per-node gather, without its shared-memory accumulator: every load
+// is independent (high memory-level parallelism) and coalesced across consecutive nodes.
+__device__ __forceinline__ int vtk_local(int lx, int ly, int lz) {  // HEX8 vertex order, mesh.py:159-167
+  return lz * 4 + (ly ? (lx ? 2 : 3) : (lx ? 1 : 0));
+}
+
+template <int VEC, bool SOA>
+__global__ void __launch_bounds__(kThreads) k_grid_pull(const double *__restrict__ Ke, int64_t n_cells, int NX,
+                                                        int NY, int NZ, int64_t gnpad, double *__restrict__ grid) {
+  constexpr int VV = VEC * VEC;
+  const int64_t nn = (int64_t)NX * NY * NZ;
+  const int cx_n = NX - 1, cy_n = NY - 1, cz_n = NZ - 1;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int kz = (int)(n / ((int64_t)NX * NY)), rem = (int)(n - (int64_t)kz * NX * NY), jy = rem / NX,
+              ix = rem - jy * NX;
+#pragma unroll 1
+    for (int q = 0; q < 14; ++q) {
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      if ((unsigned)(ix + di) >= (unsigned)NX || (unsigned)(jy + dj) >= (unsigned)NY || (unsigned)(kz + dk) >= (unsigned)NZ)
+        continue;  // no such neighbour: the SpMV masks this offset
+      double acc[VV];
+#pragma unroll
+      for (int t = 0; t < VV; ++t) acc[t] = 0.0;
+      // corner of a shared cell along an axis: offset 0 -> {x-1, x}; +1 -> x; -1 -> x-1
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+        const int cz = (dk == 0) ? kz - 1 + oz : (dk > 0 ? kz : kz - 1);
+        if ((dk != 0 && oz) || (unsigned)cz >= (unsigned)cz_n) continue;
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy) {
+          const int cy = (dj == 0) ? jy - 1 + oy : (dj > 0 ? jy : jy - 1);
+          if ((dj != 0 && oy) || (unsigned)cy >= (unsigned)cy_n) continue;
+#pragma unroll
+          for (int ox = 0; ox < 2; ++ox) {
+            const int cx = (di == 0) ? ix - 1 + ox : (di > 0 ? ix : ix - 1);
+            if ((di != 0 && ox) || (unsigned)cx >= (unsigned)cx_n) continue;
+            const int64_t cell = cx + (int64_t)cx_n * (cy + (int64_t)cy_n * cz);
+            const int a = vtk_local(ix - cx, jy - cy, kz - cz);
+            const int b = vtk_local(ix + di - cx, jy + dj - cy, kz + dk - cz);
+            const int pa = a <= b ? a : b, pb = a <= b ? b : a;
+            const int pr = c_pair_idx[pa][pb];
+            const double *src = SOA ? Ke + (int64_t)pr * VV * n_cells + cell : Ke + (cell * 36 + pr) * VV;
+#pragma unroll
+            for (int t = 0; t < VV; ++t) {
+              const int i = t / VEC, k = t - i * VEC;
+              const int off = a <= b ? t : k * VEC + i;  // block (b, a) is the transpose
+              acc[t] += __ldg(src + (SOA ? (int64_t)off * n_cells : off));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < VV; ++t) grid[grid_idx(q, t, n, gnpad, VV)] = acc[t];
+    }
+  }
+}
+
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
 int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym, double *grid) {
@@ -1174,12 +1241,30 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
   const int vv = c->vec * c->vec;
   if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
   const ElemArgs a = make_args(c, U);
+  // GRID-only tangent on a lattice: element-major scratch + lattice pull instead of the gather
+  // (element-major scratch for vec 1; vec 3 keeps the cell-major blocks, whose 72-byte rows the
+  // pull reads whole -- element-major stores of a warp-per-cell kernel would be partial sectors)
+  const bool pull = grid && !data && !sym && c->grid_nx && !getenv("B200FEM_NO_GRID_PULL");
+  const int soa = (pull && c->vec == 1) ? 1 : 0;
   const int g = grid_cap(c->n_cells, kJacWarps);
   switch (c->material) {
-    case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
-    case B200FEM_MAT_LE: k_jacobian<B200FEM_MAT_LE><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
-    case B200FEM_MAT_NH: k_jacobian<B200FEM_MAT_NH><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
-    default: k_jacobian<B200FEM_MAT_J2><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch); break;
+    case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+    case B200FEM_MAT_LE: k_jacobian<B200FEM_MAT_LE><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+    case B200FEM_MAT_NH: k_jacobian<B200FEM_MAT_NH><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+    default: k_jacobian<B200FEM_MAT_J2><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+  }
+  if (pull) {
+    const int64_t nn = c->n_nodes;
+    const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nn + kThreads - 1) / kThreads));
+    if (c->vec == 3)
+      k_grid_pull<3, false><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
+                                                    c->grid_npad, grid);
+    else
+      k_grid_pull<1, true><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
+                                                   c->grid_npad, grid);
+    count_launch(2);
+    B200_CUDA_E(cudaGetLastError(), err);
+    return fetch_element_errors(c, err, true);
   }
   int warps = 8;
   while (warps > 1 && (size_t)warps * vv * c->max_nbr * sizeof(double) > 96 * 1024) warps >>= 1;
