@@ -1234,6 +1234,73 @@ __global__ void __launch_bounds__(kThreads) k_grid_pull(const double *__restrict
   }
 }
 
+// The same lattice pull into the reference CSR layout (assemble_jacobian on box meshes): node
+// n's VEC rows hold its 27 (or fewer, at the boundary) neighbour blocks in ascending node id,
+// i.e. lexicographic (dk, dj, di); Dirichlet rows become identity rows (assembly.py:297-299).
+// Same per-slot order (ascending cell id) and values as the per-node gather.
+template <int VEC, bool SOA>
+__global__ void __launch_bounds__(kThreads) k_csr_pull(const double *__restrict__ Ke, int64_t n_cells, int NX,
+                                                       int NY, int NZ, const int32_t *__restrict__ nbr_ptr,
+                                                       const uint8_t *__restrict__ dir_flag, double *__restrict__ data) {
+  constexpr int VV = VEC * VEC;
+  const int64_t nn = (int64_t)NX * NY * NZ;
+  const int cx_n = NX - 1, cy_n = NY - 1, cz_n = NZ - 1;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
+    const int kz = (int)(n / ((int64_t)NX * NY)), rem = (int)(n - (int64_t)kz * NX * NY), jy = rem / NX,
+              ix = rem - jy * NX;
+    const int64_t p0 = __ldg(nbr_ptr + n);
+    const int cnt = __ldg(nbr_ptr + n + 1) - (int)p0, L = VEC * cnt;
+    double *rows = data + (int64_t)VV * p0;  // row c of the node at rows + c * L
+    bool dflag[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) dflag[c] = dir_flag && __ldg(dir_flag + n * VEC + c);
+    int j = 0;
+#pragma unroll 1
+    for (int o = 0; o < 27; ++o) {
+      const int dk = o / 9 - 1, dj = (o / 3) % 3 - 1, di = o % 3 - 1;
+      if ((unsigned)(ix + di) >= (unsigned)NX || (unsigned)(jy + dj) >= (unsigned)NY || (unsigned)(kz + dk) >= (unsigned)NZ)
+        continue;
+      double acc[VV];
+#pragma unroll
+      for (int t = 0; t < VV; ++t) acc[t] = 0.0;
+#pragma unroll
+      for (int oz = 0; oz < 2; ++oz) {
+        const int cz = (dk == 0) ? kz - 1 + oz : (dk > 0 ? kz : kz - 1);
+        if ((dk != 0 && oz) || (unsigned)cz >= (unsigned)cz_n) continue;
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy) {
+          const int cy = (dj == 0) ? jy - 1 + oy : (dj > 0 ? jy : jy - 1);
+          if ((dj != 0 && oy) || (unsigned)cy >= (unsigned)cy_n) continue;
+#pragma unroll
+          for (int ox = 0; ox < 2; ++ox) {
+            const int cx = (di == 0) ? ix - 1 + ox : (di > 0 ? ix : ix - 1);
+            if ((di != 0 && ox) || (unsigned)cx >= (unsigned)cx_n) continue;
+            const int64_t cell = cx + (int64_t)cx_n * (cy + (int64_t)cy_n * cz);
+            const int a = vtk_local(ix - cx, jy - cy, kz - cz);
+            const int b = vtk_local(ix + di - cx, jy + dj - cy, kz + dk - cz);
+            const int pa = a <= b ? a : b, pb = a <= b ? b : a;
+            const int pr = c_pair_idx[pa][pb];
+            const double *src = SOA ? Ke + (int64_t)pr * VV * n_cells + cell : Ke + (cell * 36 + pr) * VV;
+#pragma unroll
+            for (int t = 0; t < VV; ++t) {
+              const int i = t / VEC, k = t - i * VEC;
+              const int off = a <= b ? t : k * VEC + i;
+              acc[t] += __ldg(src + (SOA ? (int64_t)off * n_cells : off));
+            }
+          }
+        }
+      }
+      const bool self = (o == 13);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+          rows[c * L + VEC * j + k] = dflag[c] ? ((self && k == c) ? 1.0 : 0.0) : acc[c * VEC + k];
+      ++j;
+    }
+  }
+}
+
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
 int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym, double *grid) {
@@ -1245,7 +1312,11 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
   // (element-major scratch for vec 1; vec 3 keeps the cell-major blocks, whose 72-byte rows the
   // pull reads whole -- element-major stores of a warp-per-cell kernel would be partial sectors)
   const bool pull = grid && !data && !sym && c->grid_nx && !getenv("B200FEM_NO_GRID_PULL");
-  const int soa = (pull && c->vec == 1) ? 1 : 0;
+  // reference CSR layout on a scalar lattice: the same pull (assemble_jacobian, operator="csr").
+  // Not for vec 3: a thread's 27 blocks land in 3 rows ~2 KB apart from its neighbours' -- the
+  // uncoalesced 8-byte stores made it 21 ms against 13.7 ms for the gather (config 3)
+  const bool csr_pull = !grid && data && !sym && c->grid_nx && c->vec == 1 && !getenv("B200FEM_NO_GRID_PULL");
+  const int soa = ((pull || csr_pull) && c->vec == 1) ? 1 : 0;
   const int g = grid_cap(c->n_cells, kJacWarps);
   switch (c->material) {
     case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
@@ -1262,6 +1333,16 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
     else
       k_grid_pull<1, true><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
                                                    c->grid_npad, grid);
+    count_launch(2);
+    B200_CUDA_E(cudaGetLastError(), err);
+    return fetch_element_errors(c, err, true);
+  }
+  if (csr_pull) {
+    const int64_t nn = c->n_nodes;
+    const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nn + kThreads - 1) / kThreads));
+    const uint8_t *df = c->n_dir ? c->dir_flag : nullptr;
+    k_csr_pull<1, true><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
+                                                c->nbr_ptr, df, data);
     count_launch(2);
     B200_CUDA_E(cudaGetLastError(), err);
     return fetch_element_errors(c, err, true);
