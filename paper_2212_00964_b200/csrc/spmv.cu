@@ -913,6 +913,15 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
     if (node < node_lo || node >= node_hi) continue;
     const LatticePos p = lattice_pos(node, c0, g);
     const double *__restrict__ x = a.x;
+    // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
+    // their latency hides behind the 27 block products instead of trailing them
+    RowPre pre[3];
+    bool dfl[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      pre[r] = spmv_preload<MODE>(3 * (int64_t)node + r, a);
+      dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
+    }
     double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
@@ -949,9 +958,8 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int64_t row = 3 * (int64_t)node + r;
-      const RowPre pre = spmv_preload<MODE>(row, a);
-      const double acc = (dir_flag && __ldg(dir_flag + row)) ? __ldg(x + row) : yu[r] + yl[r];
-      spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+      const double acc = dfl[r] ? __ldg(x + row) : yu[r] + yl[r];
+      spmv_epilogue<MODE>(row, acc, a, pre[r], red0, red1);
     }
   }
   if (MODE != SP_PLAIN) {
