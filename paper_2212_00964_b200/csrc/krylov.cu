@@ -156,53 +156,65 @@ static bool use_graph_loop() {
   return v == 1;
 }
 
-// Build (once per solve start: x and b may differ between calls) and run the while-graph of
-// `enqueue` on the matrix's stream; returns 0 or a CUDA error.
+// The while-graph of `enqueue` is built once per solve (x and b differ between calls) and
+// relaunched on the matrix's stream at every (re)start of that solve: restart-heavy solves
+// (BiCGSTAB breakdowns near the round-off floor) do not pay a graph instantiation per restart.
+struct LoopGraph {
+  cudaGraphExec_t exec = nullptr;
+  ~LoopGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 template <class F>
-static int run_loop_graph(Matrix *m, F &&enqueue, b200fem_error *err) {
+static int run_loop_graph(Matrix *m, LoopGraph &lg, F &&enqueue, b200fem_error *err) {
   KrylovWork *w = m->kw;
   cudaStream_t s = m->stream;
-  // capture needs a non-default stream (the caller's may be the legacy stream): the body is
-  // captured on a private stream, the graph then runs on the matrix's stream
-  static thread_local cudaStream_t cs = nullptr;
-  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return cuda_status(cudaGetLastError(), err, "capture stream");
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t ge = nullptr;
-  cudaGraphConditionalHandle h;
   cudaError_t e = cudaSuccess;
-  const char *where = "";
-  do {
-    where = "cudaGraphCreate";
-    if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) break;
-    where = "cudaGraphConditionalHandleCreate";
-    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) break;
-    cudaGraphNodeParams np{};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    where = "cudaGraphAddNode(while)";
-    if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np)) != cudaSuccess) break;
-    cudaGraph_t body = np.conditional.phGraph_out[0];
-    where = "cudaStreamBeginCaptureToGraph";
-    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
-      break;
-    m->stream = cs;
-    enqueue();
-    k_loop_cond<<<1, 1, 0, cs>>>(h, w->sc);
+  const char *where = "cudaGraphLaunch";
+  if (!lg.exec) {
+    // capture needs a non-default stream (the caller's may be the legacy stream): the body is
+    // captured on a private stream, the graph then runs on the matrix's stream
+    static thread_local cudaStream_t cs = nullptr;
+    if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), err, "capture stream");
+    cudaGraph_t g = nullptr;
+    cudaGraphConditionalHandle h;
+    do {
+      where = "cudaGraphCreate";
+      if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) break;
+      where = "cudaGraphConditionalHandleCreate";
+      if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) break;
+      cudaGraphNodeParams np{};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      where = "cudaGraphAddNode(while)";
+      if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np)) != cudaSuccess) break;
+      cudaGraph_t body = np.conditional.phGraph_out[0];
+      where = "cudaStreamBeginCaptureToGraph";
+      if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) !=
+          cudaSuccess)
+        break;
+      m->stream = cs;
+      enqueue();
+      k_loop_cond<<<1, 1, 0, cs>>>(h, w->sc);
+      m->stream = s;
+      cudaGraph_t cap = nullptr;
+      where = "cudaStreamEndCapture";
+      if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) break;
+      where = "cudaGraphInstantiate";
+      if ((e = cudaGraphInstantiate(&lg.exec, g, 0)) != cudaSuccess) break;
+    } while (false);
     m->stream = s;
-    cudaGraph_t cap = nullptr;
-    where = "cudaStreamEndCapture";
-    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) break;
-    where = "cudaGraphInstantiate";
-    if ((e = cudaGraphInstantiate(&ge, g, 0)) != cudaSuccess) break;
+    if (g) cudaGraphDestroy(g);
+  }
+  if (e == cudaSuccess) {
     where = "cudaGraphLaunch";
-    if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) break;
-  } while (false);
-  m->stream = s;
-  if (ge) cudaGraphExecDestroy(ge);  // deferred until the launch completes
-  if (g) cudaGraphDestroy(g);
+    e = cudaGraphLaunch(lg.exec, s);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_err(err, B200FEM_E_CUDA, "Krylov while-graph: %s failed: %s", where, cudaGetErrorString(e));
@@ -263,6 +275,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
   long long it = 0, mv = 0, restarts = 0;
   double last_bd = -1.0;
   const size_t ssz = sizeof(KrylovScalars);
+  LoopGraph loop_graph;  // built at the first inner loop, relaunched at every restart
   for (;;) {
     // ---- (re)start: r = D^-1 (b - A x), r0 = r, res = ||D r||   (solvers.py:115-118)
     H[0].status = KS_RUNNING;
@@ -301,7 +314,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     KrylovScalars done{};
     if (use_graph_loop()) {
       const long long it0 = it;
-      if (int rc = run_loop_graph(m, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
+      if (int rc = run_loop_graph(m, loop_graph, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
       B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
       B200_CUDA_E(cudaStreamSynchronize(s), err);
       count_launch(5 * (H[1].it - it0) + 1);
@@ -395,6 +408,7 @@ int pcg(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, doubl
   H[0].max_iters = max_it;
   long long it = 0, mv = 0, restarts = 0;
   const size_t ssz = sizeof(KrylovScalars);
+  LoopGraph loop_graph;
   for (;;) {
     H[0].status = KS_RUNNING;
     H[0].it = it;
@@ -423,7 +437,7 @@ int pcg(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, doubl
     int cur = 0;
     if (use_graph_loop()) {
       const long long it0 = it;
-      if (int rc = run_loop_graph(m, [&] { enqueue_cg_iteration(m, x); }, err)) return rc;
+      if (int rc = run_loop_graph(m, loop_graph, [&] { enqueue_cg_iteration(m, x); }, err)) return rc;
       B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
       B200_CUDA_E(cudaStreamSynchronize(s), err);
       count_launch(3 * (H[1].it - it0) + 1);
