@@ -1,0 +1,225 @@
+"""Ports of the reference's own assembly / solver / acceptance tests (reference
+pkg/tests/test_assembly.py, test_solvers.py, test_acceptance.py), run against this package:
+every assembly, matvec and Krylov solve below goes through libb200fem on the GPU.  Same
+inputs, same assertions and tolerances as the reference tests (file:line in each docstring)."""
+
+import numpy as np
+import pytest
+
+import paper_2212_00964_b200 as fem
+from paper_2212_00964_b200 import (BoundaryLocator, DirichletSpec, LinearElasticityProblem, LoadSchedule,
+                                   NeoHookeanProblem, NewtonConfig, PoissonProblem, J2PlasticityProblem,
+                                   assemble_jacobian, assemble_residual, generate_box_mesh, impose_dirichlet_residual,
+                                   incremental_solve, locate_nodes, newton_solve, workspace)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def aluminum():
+    return fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=250.0)
+
+
+def onbox_locator(Lx, Ly, Lz, tol=1e-9):  # reference tests/conftest.py:9-19
+    def pred(p):
+        p = np.asarray(p)
+        return ((np.abs(p[..., 0]) < tol) | (np.abs(p[..., 0] - Lx) < tol) | (np.abs(p[..., 1]) < tol)
+                | (np.abs(p[..., 1] - Ly) < tol) | (np.abs(p[..., 2]) < tol) | (np.abs(p[..., 2] - Lz) < tol))
+    return BoundaryLocator(pred)
+
+
+def affine_dirichlet(A, locator):  # reference tests/conftest.py:22-30
+    A = np.asarray(A, dtype=np.float64)
+    return [DirichletSpec(locator, c, (lambda c: lambda p: (np.atleast_2d(p) @ A.T)[..., c])(c)) for c in range(3)]
+
+
+def zero_dirichlet(locator, vec=3):  # reference tests/conftest.py:33-34
+    return [DirichletSpec(locator, c, lambda p: 0.0) for c in range(vec)]
+
+
+def fd_jacobian(problem, U, h=1e-6):  # reference test_assembly.py:26-33
+    n = U.shape[0]
+    cols = np.zeros((n, n))
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = h
+        cols[:, j] = (assemble_residual(problem, U + e) - assemble_residual(problem, U - e)) / (2 * h)
+    return cols
+
+
+def test_patch_equilibrium_interior_rows_vanish(aluminum):
+    """test_assembly.py:36-44"""
+    mesh = generate_box_mesh(3, 3, 3, 1, 1, 1)
+    A = np.array([[0.01, 0.004, 0.002], [0.0, -0.005, 0.003], [0.001, 0.0, 0.007]])
+    prob = LinearElasticityProblem(mesh, aluminum, [])
+    R = assemble_residual(prob, (mesh.nodes @ A.T).ravel())
+    interior = np.setdiff1d(np.arange(mesh.n_nodes), locate_nodes(mesh, onbox_locator(1, 1, 1)))
+    idofs = (interior[:, None] * 3 + np.arange(3)).ravel()
+    assert np.abs(R[idofs]).max() < 1e-10
+
+
+def test_dirichlet_row_overwrite(aluminum):
+    """test_assembly.py:47-59"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    prob = LinearElasticityProblem(mesh, aluminum, [DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.1)])
+    ws = workspace(prob)
+    U = np.zeros(prob.n_dofs)
+    assert np.allclose(assemble_residual(prob, U)[ws.dir_dofs], -0.1)
+    U[ws.dir_dofs] = 0.1
+    assert np.allclose(assemble_residual(prob, U)[ws.dir_dofs], 0.0)
+
+
+def test_impose_dirichlet_residual_op():
+    """test_assembly.py:62-72"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    R = np.arange(24, dtype=np.float64)
+    U = np.zeros(24)
+    assert np.array_equal(impose_dirichlet_residual(R, U, mesh, 3, []), R)
+    specs = [DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.1)]
+    out2 = impose_dirichlet_residual(R, U, mesh, 3, specs)
+    nodes = locate_nodes(mesh, BoundaryLocator.plane(2, 1.0))
+    assert np.allclose(out2[nodes * 3 + 2], -0.1)
+
+
+def test_duplicate_consistent_constraints_allowed(aluminum):
+    """test_assembly.py:90-95"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    top = BoundaryLocator.plane(2, 1.0)
+    prob = LinearElasticityProblem(mesh, aluminum, [DirichletSpec(top, 2, lambda p: 0.1),
+                                                     DirichletSpec(top, 2, lambda p: 0.1)])
+    assemble_residual(prob, np.zeros(prob.n_dofs))
+
+
+def test_constant_body_force_load_single_cell():
+    """test_assembly.py:98-103"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    c = 3.7
+    prob = PoissonProblem(mesh, alpha=1.0, dirichlet=[], source=lambda p: np.full(np.asarray(p).shape[:-1] + (1,), c))
+    assert np.allclose(assemble_residual(prob, np.zeros(8)), -c / 8.0, rtol=1e-13)
+
+
+def test_linear_jacobian_independent_of_state(aluminum, rng):
+    """test_assembly.py:106-112"""
+    mesh = generate_box_mesh(2, 2, 1, 1, 1, 1)
+    prob = LinearElasticityProblem(mesh, aluminum, zero_dirichlet(BoundaryLocator.plane(2, 0.0)))
+    K1 = assemble_jacobian(prob, rng.standard_normal(prob.n_dofs) * 0.01)
+    prob._jac_cache = None
+    K2 = assemble_jacobian(prob, rng.standard_normal(prob.n_dofs) * 0.01)
+    assert np.array_equal(K1.data, K2.data)
+
+
+def _shape_gradients(xi):  # d phi_k / d xi for the HEX8 vertex order (reference elements.py:38-53)
+    s = np.array([[-1, -1, -1], [1, -1, -1], [1, 1, -1], [-1, 1, -1], [-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]],
+                 dtype=np.float64)
+    t = 1.0 + s * xi
+    return np.stack([s[:, 0] * t[:, 1] * t[:, 2], s[:, 1] * t[:, 0] * t[:, 2], s[:, 2] * t[:, 0] * t[:, 1]], axis=1) / 8
+
+
+def test_poisson_single_cell_matrix_matches_oracle():
+    """test_assembly.py:115-138: an independent 3x3x3-Gauss dense oracle of the unit cell."""
+    pts, wts = np.array([-np.sqrt(0.6), 0.0, np.sqrt(0.6)]), np.array([5.0, 8.0, 5.0]) / 9.0
+    Ko = np.zeros((8, 8))
+    for a, wa in zip(pts, wts):
+        for b, wb in zip(pts, wts):
+            for c, wc in zip(pts, wts):
+                g = _shape_gradients(np.array([a, b, c])) * 2.0
+                Ko += wa * wb * wc * (g @ g.T) / 8.0
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    K = assemble_jacobian(PoissonProblem(mesh, alpha=1.0, dirichlet=[]), np.zeros(8)).todense()
+    loc = mesh.cells[0]
+    assert np.allclose(K[np.ix_(loc, loc)], Ko, atol=1e-14)
+    assert np.abs(K.sum(axis=1)).max() < 1e-14
+
+
+def test_all_dirichlet_gives_identity(aluminum):
+    """test_assembly.py:141-147"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    prob = LinearElasticityProblem(mesh, aluminum, zero_dirichlet(BoundaryLocator.everywhere()))
+    assert np.array_equal(assemble_jacobian(prob, np.zeros(prob.n_dofs)).todense(), np.eye(prob.n_dofs))
+
+
+@pytest.mark.parametrize("kind", ["linear", "neo_hookean", "j2"])
+def test_jacobian_matches_finite_differences(kind, aluminum, rng):
+    """test_assembly.py:150-169: the hand-derived device tangents against central FD of the
+    device residual (the reference checks its AD Jacobian the same way)."""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    specs = affine_dirichlet(0.001 * np.eye(3), onbox_locator(*mesh.nodes.max(axis=0)))
+    cls = {"linear": LinearElasticityProblem, "neo_hookean": NeoHookeanProblem, "j2": J2PlasticityProblem}[kind]
+    prob = cls(mesh, aluminum, specs)
+    U = 0.002 * rng.standard_normal(prob.n_dofs)
+    K = assemble_jacobian(prob, U).todense()
+    K_fd = fd_jacobian(prob, U)
+    pattern = K_fd != 0.0
+    assert np.abs(K - K_fd)[pattern].max() / np.abs(K_fd).max() < 1e-6
+
+
+def test_linear_elastic_global_symmetry(aluminum):
+    """test_assembly.py:172-180"""
+    mesh = generate_box_mesh(3, 2, 2, 1, 1, 1)
+    prob = LinearElasticityProblem(mesh, aluminum, zero_dirichlet(BoundaryLocator.plane(2, 0.0)))
+    K = assemble_jacobian(prob, np.zeros(prob.n_dofs)).todense()
+    free = np.setdiff1d(np.arange(prob.n_dofs), workspace(prob).dir_dofs)
+    Kf = K[np.ix_(free, free)]
+    assert np.abs(Kf - Kf.T).max() <= 1e-10 * np.abs(Kf).max()
+
+
+def test_assembly_deterministic(aluminum, rng):
+    """test_assembly.py:183-194"""
+    mesh = generate_box_mesh(3, 3, 2, 1, 1, 1)
+    prob = LinearElasticityProblem(mesh, aluminum, zero_dirichlet(BoundaryLocator.plane(2, 0.0)))
+    prob.jacobian_constant = False
+    U = 0.01 * rng.standard_normal(prob.n_dofs)
+    assert np.array_equal(assemble_jacobian(prob, U).data, assemble_jacobian(prob, U).data)
+    assert np.array_equal(assemble_residual(prob, U), assemble_residual(prob, U))
+
+
+def test_newton_linear_one_iteration(aluminum):
+    """test_solvers.py:101-110"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    specs = zero_dirichlet(BoundaryLocator.plane(2, 0.0)) + [
+        DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.01)]
+    U, rep = newton_solve(LinearElasticityProblem(mesh, aluminum, specs))
+    assert rep.n_iterations == 1 and len(rep.residual_norms) == 2
+    assert rep.residual_norms[1] <= 1e-10 * rep.residual_norms[0]
+
+
+def test_newton_superlinear_contraction(aluminum):
+    """test_solvers.py:113-123"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    specs = zero_dirichlet(BoundaryLocator.plane(2, 0.0)) + [
+        DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.02)]
+    _, rep = newton_solve(NeoHookeanProblem(mesh, aluminum, specs), cfg=NewtonConfig(rel_tol=1e-9, abs_tol=1e-10))
+    norms = np.array(rep.residual_norms)
+    below = norms[(norms < 1.0) & (norms > 1e-13)]
+    assert below.size >= 2
+    assert np.log(below[-1]) / np.log(below[-2]) >= 1.5
+
+
+def test_newton_all_dirichlet(aluminum):
+    """test_solvers.py:126-134"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    A = np.diag([0.01, -0.005, 0.02])
+    U, rep = newton_solve(LinearElasticityProblem(mesh, aluminum, affine_dirichlet(A, BoundaryLocator.everywhere())))
+    assert rep.n_iterations == 1
+    assert np.allclose(U, (mesh.nodes @ A.T).ravel(), atol=1e-14)
+
+
+def test_incremental_elastic_path_independence(aluminum):
+    """test_solvers.py:164-173 and test_acceptance.py:341-355 (criterion 10)."""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    top = BoundaryLocator.plane(2, 1.0)
+    specs = zero_dirichlet(BoundaryLocator.plane(2, 0.0)) + [DirichletSpec(top, 2, lambda p: 0.05)]
+    ha = incremental_solve(LinearElasticityProblem(mesh, aluminum, specs), LoadSchedule.ramp(2), reaction_locator=top)
+    hb = incremental_solve(LinearElasticityProblem(mesh, aluminum, specs), LoadSchedule.ramp(10), reaction_locator=top)
+    assert np.abs(ha.steps[-1].U - hb.steps[-1].U).max() < 1e-8
+    assert abs(ha.steps[-1].reaction - hb.steps[-1].reaction) / abs(hb.steps[-1].reaction) < 1e-8
+
+
+def test_incremental_zero_schedule(aluminum):
+    """test_solvers.py:176-184"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    specs = zero_dirichlet(BoundaryLocator.plane(2, 0.0)) + [
+        DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.05)]
+    hist = incremental_solve(LinearElasticityProblem(mesh, aluminum, specs), LoadSchedule((0.0, 0.0, 0.0)))
+    for rec in hist.steps:
+        assert np.abs(rec.U).max() == 0.0
