@@ -40,6 +40,10 @@ struct Part {
   // their SpMV runs on s2 while the halo is exchanged; the two boundary bands follow it
   bool overlap = false;
   int64_t int_lo = 0, int_hi = 0;
+  // every peer's send and recv node list is a contiguous local range (plane-cut lattices):
+  // the halo then moves vector slices directly -- no pack / unpack kernels
+  bool contiguous = false;
+  std::vector<int64_t> s_lo, r_lo;
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
   RedScratch red_in{}, red_lo{}, red_hi{};  // partial dot totals of the three launches
@@ -111,7 +115,7 @@ struct Dist {
     for (size_t p = 0; p < parts.size(); ++p) {
       Part *P = parts[p];
       const int64_t ns = P->soff.back();
-      if (ns) {
+      if (ns && !P->contiguous) {
         k_pack<<<grid_n(ns * P->vec), kThreads, 0, stream(p)>>>(vec[p], P->send_nodes, ns, P->vec, P->sendbuf);
         count_launch();
       }
@@ -122,8 +126,10 @@ struct Dist {
         ncclGroupStart();
         for (int i = 0; i < P->n_peers; ++i) {
           const int64_t sn = P->soff[i + 1] - P->soff[i], rn = P->roff[i + 1] - P->roff[i];
-          if (sn) ncclSend(P->sendbuf + P->soff[i] * P->vec, sn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
-          if (rn) ncclRecv(P->recvbuf + P->roff[i] * P->vec, rn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
+          const double *sp = P->contiguous ? vec[0] + P->s_lo[i] * P->vec : P->sendbuf + P->soff[i] * P->vec;
+          double *rp = P->contiguous ? vec[0] + P->r_lo[i] * P->vec : P->recvbuf + P->roff[i] * P->vec;
+          if (sn) ncclSend(sp, sn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
+          if (rn) ncclRecv(rp, rn * P->vec, ncclDouble, P->peer[i], comm->nccl, stream(0));
         }
         if (ncclGroupEnd() != ncclSuccess) return B200FEM_E_CUDA;
       }
@@ -137,16 +143,16 @@ struct Dist {
           if (j == Q->n_peers) return B200FEM_E_INVALID;
           const int64_t rn = P->roff[i + 1] - P->roff[i];
           if (rn != Q->soff[j + 1] - Q->soff[j]) return B200FEM_E_INVALID;
-          if (rn)
-            B200_CUDA(cudaMemcpyAsync(P->recvbuf + P->roff[i] * P->vec, Q->sendbuf + Q->soff[j] * Q->vec,
-                                      rn * P->vec * sizeof(double), cudaMemcpyDeviceToDevice, stream(p)));
+          const double *sp = Q->contiguous ? vec[P->peer[i]] + Q->s_lo[j] * Q->vec : Q->sendbuf + Q->soff[j] * Q->vec;
+          double *rp = P->contiguous ? vec[p] + P->r_lo[i] * P->vec : P->recvbuf + P->roff[i] * P->vec;
+          if (rn) B200_CUDA(cudaMemcpyAsync(rp, sp, rn * P->vec * sizeof(double), cudaMemcpyDeviceToDevice, stream(p)));
         }
       }
     }
     for (size_t p = 0; p < parts.size(); ++p) {
       Part *P = parts[p];
       const int64_t nr = P->roff.back();
-      if (nr) {
+      if (nr && !P->contiguous) {
         k_unpack<<<grid_n(nr * P->vec), kThreads, 0, stream(p)>>>(vec[p], P->recv_nodes, nr, P->vec, P->recvbuf);
         count_launch();
       }
@@ -481,6 +487,20 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
   }
   if (ns) cudaMemcpy(P->send_nodes, send_nodes, ns * sizeof(int32_t), cudaMemcpyHostToDevice);
   if (nr) cudaMemcpy(P->recv_nodes, recv_nodes, nr * sizeof(int32_t), cudaMemcpyHostToDevice);
+  // contiguous halo lists (checked on the host lists)
+  auto run = [](const int32_t *v, int64_t lo, int64_t hi) {
+    for (int64_t t = lo + 1; t < hi; ++t)
+      if (v[t] != v[t - 1] + 1) return false;
+    return true;
+  };
+  P->contiguous = !getenv("B200FEM_HALO_PACK");
+  for (int i = 0; i < n_peers && P->contiguous; ++i)
+    P->contiguous = run(send_nodes, P->soff[i], P->soff[i + 1]) && run(recv_nodes, P->roff[i], P->roff[i + 1]);
+  if (P->contiguous)
+    for (int i = 0; i < n_peers; ++i) {
+      P->s_lo.push_back(P->soff[i + 1] > P->soff[i] ? send_nodes[P->soff[i]] : 0);
+      P->r_lo.push_back(P->roff[i + 1] > P->roff[i] ? recv_nodes[P->roff[i]] : 0);
+    }
   *out = (b200fem_part *)P;
   return 0;
 }
