@@ -874,6 +874,7 @@ constexpr int kGMinBlocks = 1;  // 255 registers: ILP per thread beats more warp
 struct GridDims {
   int nx, ny, nz, nxy, nn;  // nodes per axis, per plane, total
   int64_t npad;             // element-array length
+  int slab;                 // rows per slab of the slab-major traversal (0: plain node order)
 };
 
 struct LatticePos {  // which faces of the lattice node a lies on
@@ -896,6 +897,48 @@ __device__ __forceinline__ bool grid_has(const LatticePos &p, int di, int dj, in
            (dk > 0 && p.kN));
 }
 
+// Traversal order of the GRID3 matvec.  Every upper block of node m is read a second time,
+// transposed, by node m + off as one of its lower blocks; in plain node order 9 of the 13
+// offsets span a whole lattice plane, so that second read comes one plane (+ one wave of
+// 148 x 256 nodes) later and misses L2 once the plane outgrows it (ncu DRAM bytes over the
+// algorithmic bytes: +3 % at 136^3, +18 % at 160^3, +40 % at 200^3).  Slab-major order walks
+// slabs of `slab` rows through all planes (for s: for k: rows [s*slab, (s+1)*slab) of plane
+// k), which bounds the reuse distance by slab * nx nodes for any lattice size; only the
+// first / last row of a slab re-reads across the slab boundary.  Work item w is a (slab,
+// plane) segment and a chunk slot in it; a chunk straddling two segments is visited by both,
+// each lane keeping only its own segment's nodes.
+struct SlabWalk {
+  int64_t n_work;
+  int per_seg, nk, klo;
+  __device__ __forceinline__ int chunk(int64_t w, const GridDims &g, int node_lo, int node_hi, int &lo,
+                                       int &hi) const {
+    if (g.slab == 0) {  // plain order: chunk c_lo + w over [node_lo, node_hi)
+      lo = node_lo, hi = node_hi;
+      return (node_lo >> 5) + (int)w;
+    }
+    const int seg = (int)(w / per_seg), slot = (int)(w - (int64_t)seg * per_seg);
+    const int s = seg / nk, k = klo + (seg - s * nk);
+    const int row0 = s * g.slab, row1 = min(row0 + g.slab, g.ny);
+    lo = max(node_lo, k * g.nxy + row0 * g.nx);
+    hi = min(node_hi, k * g.nxy + row1 * g.nx);
+    const int c = (lo >> 5) + slot;
+    if (lo >= hi || c > ((hi - 1) >> 5)) hi = lo;  // empty slot: no lane passes the range test
+    return c;
+  }
+};
+__device__ __forceinline__ SlabWalk slab_walk(const GridDims &g, int node_lo, int node_hi) {
+  SlabWalk sw{};
+  if (g.slab == 0) {
+    sw.n_work = ((node_hi + 31) >> 5) - (node_lo >> 5);
+    return sw;
+  }
+  sw.klo = node_lo / g.nxy;
+  sw.nk = (node_hi - 1) / g.nxy + 1 - sw.klo;
+  sw.per_seg = (g.slab * g.nx + 31) / 32 + 1;
+  sw.n_work = (int64_t)((g.ny + g.slab - 1) / g.slab) * sw.nk * sw.per_seg;
+  return sw;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const double *__restrict__ grid, GridDims g,
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
@@ -904,13 +947,15 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
   const int lane = threadIdx.x & 31;
   const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const int c_lo = node_lo >> 5, n_chunks = (node_hi + 31) >> 5;  // rows of nodes [node_lo, node_hi)
   const int64_t np = g.npad;
   double red0 = 0.0, red1 = 0.0;
   const int nch = (int)(np >> 5);
-  for (int c = c_lo + warp0; c < n_chunks; c += nwarps) {
+  const SlabWalk sw = slab_walk(g, node_lo, node_hi);
+  for (int64_t w = warp0; w < sw.n_work; w += nwarps) {
+    int lo, hi;
+    const int c = sw.chunk(w, g, node_lo, node_hi, lo, hi);
     const int c0 = c << 5, node = c0 + lane;
-    if (node < node_lo || node >= node_hi) continue;
+    if (node < lo || node >= hi) continue;
     const LatticePos p = lattice_pos(node, c0, g);
     const double *__restrict__ x = a.x;
     // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
@@ -1020,6 +1065,16 @@ __global__ void __launch_bounds__(kGThreads, 4) k_spmv_grid1(const double *__res
 static GridDims grid_dims(const Matrix *m) {
   GridDims g{};
   g.nx = m->gnx, g.ny = m->gny, g.nz = m->gnz, g.nxy = m->gnx * m->gny, g.nn = (int)(m->n / m->gvec), g.npad = m->gnpad;
+  g.slab = 0;
+  if (m->gvec == 3) {  // slabs of ~4096 nodes per plane, once the plane is larger than 4 slabs
+    static int env = -2;
+    if (env == -2) {
+      const char *e = getenv("B200FEM_GRID_SLAB");
+      env = e ? atoi(e) : -1;
+    }
+    const int rows = env >= 0 ? env : (4096 + g.nx - 1) / g.nx;
+    if (rows > 0 && (env >= 0 || g.ny >= 4 * rows)) g.slab = std::min(rows, g.ny);
+  }
   return g;
 }
 
