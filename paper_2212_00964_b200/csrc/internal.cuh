@@ -62,7 +62,7 @@ struct RedScratch {
 };
 
 // Krylov scalars live on the device so the inner loop never waits on the host.
-enum : int { KS_RUNNING = 0, KS_CONV_INNER = 1, KS_BREAKDOWN = 2, KS_MAXED = 3, KS_FAULT = 4 };
+enum : int { KS_RUNNING = 0, KS_CONV_INNER = 1, KS_BREAKDOWN = 2, KS_MAXED = 3 };
 struct KrylovScalars {
   double rho, alpha, omega, beta;
   double r0v, tt, ts;
@@ -131,7 +131,6 @@ struct KrylovWork {
   int64_t n = 0;
   double *r = nullptr, *r0 = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr;
   double *diag = nullptr, *inv = nullptr;
-  double *q = nullptr, *mv = nullptr;  // matvec-pair iteration: M r and M v
   KrylovScalars *sc = nullptr;
   KrylovScalars *sc_host = nullptr;  // pinned
   RedScratch red{};
@@ -165,9 +164,6 @@ struct Matrix {
   const uint8_t *dir_flag = nullptr;
   // GRID3: lattice nodes per axis and the padded offset-array length (data = 14 arrays)
   int gnx = 0, gny = 0, gnz = 0, gvec = 3;
-  unsigned long long *pair_cnt = nullptr;  // GRID3 matvec pair: segment counters, epoch, fault flag
-  int pair_nseg = 0;
-  bool use_pair = false;  // set per BiCGSTAB solve
   int64_t gnpad = 0;
 };
 
@@ -228,9 +224,6 @@ struct SpmvArgs {
                      // 0: totals are left in red.result for a cross-rank allreduce
 };
 int launch_spmv(const Matrix *m, SpmvMode mode, const SpmvArgs &a, RedScratch *red);
-bool grid3_pair_supported(const Matrix *m);
-int launch_grid3_pair(Matrix *m, const double *p, const double *r, const double *inv, const double *r0, double *v,
-                      double *q, double *w, KrylovScalars *sc, RedScratch *red);
 int launch_diagonal(const Matrix *m, double *diag, double *inv, RedScratch *red, int64_t *n_zero);
 int prepare_fem3_chunks(Matrix *m, int64_t node_lo = 0, int64_t node_hi = -1);
 int prepare_sym3_chunks(Matrix *m);

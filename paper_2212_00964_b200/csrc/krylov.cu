@@ -52,27 +52,6 @@ __global__ void __launch_bounds__(kThreads) k_update_s(int64_t n, const double *
     s[i] = r[i] - alpha * v[i];
 }
 
-// Matvec-pair iteration: s = r - alpha v and t = q - alpha w (= M s up to rounding), with the
-// dots t.t and t.s of the omega stage (solvers.py:141-150).
-__global__ void __launch_bounds__(kThreads) k_update_st(int64_t n, const double *__restrict__ r,
-                                                        const double *__restrict__ v, const double *__restrict__ q,
-                                                        const double *__restrict__ mv, double *__restrict__ s,
-                                                        double *__restrict__ t, KrylovScalars *S, RedScratch red) {
-  if (S->status != KS_RUNNING) return;
-  const double alpha = S->alpha;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double si = r[i] - alpha * v[i];
-    const double ti = q[i] - alpha * mv[i];
-    s[i] = si;
-    t[i] = ti;
-    acc[0] = fma(ti, ti, acc[0]);
-    acc[1] = fma(ti, si, acc[1]);
-  }
-  double tot[2];
-  if (block_partials_and_finish<2>(acc, red, tot) && threadIdx.x == 0) apply_stage(ST_TT, S, tot);
-}
-
 __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__restrict__ x, double *__restrict__ r,
                                                         const double *__restrict__ p, const double *__restrict__ s,
                                                         const double *__restrict__ t, const double *__restrict__ r0,
@@ -150,9 +129,8 @@ int ensure_work(Matrix *m) {
 
 void free_work(KrylovWork *w) {
   if (!w) return;
-  double *vecs[] = {w->r, w->r0, w->p, w->v, w->s, w->t, w->diag, w->inv, w->q, w->mv};
-  for (double *v : vecs)
-    if (v) cudaFree(v);
+  double *vecs[] = {w->r, w->r0, w->p, w->v, w->s, w->t, w->diag, w->inv};
+  for (double *v : vecs) cudaFree(v);
   cudaFree(w->sc);
   cudaFreeHost(w->sc_host);
   red_free(&w->red);
@@ -247,37 +225,7 @@ static int run_loop_graph(Matrix *m, LoopGraph &lg, F &&enqueue, b200fem_error *
 
 static int grid_vec(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
 
-// BiCGSTAB iteration on the GRID3 matvec pair (one matrix pass for both matvecs; see
-// k_grid3_pair in spmv.cu).  Same scalar stages as the two-matvec iteration.
-static bool pair_wanted(const Matrix *m) {  // read per solve, so tests can A/B in one process
-  const char *e = getenv("B200FEM_PAIR");
-  return (e ? atoi(e) : 0) == 1 && grid3_pair_supported(m);
-}
-
-static int ensure_pair_work(Matrix *m) {
-  KrylovWork *w = m->kw;
-  if (!w->q) B200_CUDA(dalloc(&w->q, m->n));
-  if (!w->mv) B200_CUDA(dalloc(&w->mv, m->n));
-  if (m->pair_cnt) {  // clear a fault left by an earlier solve
-    const int nseg = m->pair_nseg;
-    B200_CUDA(cudaMemsetAsync((int *)(m->pair_cnt + nseg + 1), 0, sizeof(int), m->stream));
-  }
-  return 0;
-}
-
-static void enqueue_iteration_pair(Matrix *m, double *x) {
-  KrylovWork *w = m->kw;
-  cudaStream_t s = m->stream;
-  const int64_t n = m->n;
-  k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
-  launch_grid3_pair(m, w->p, w->r, w->inv, w->r0, w->v, w->q, w->mv, w->sc, &w->red);
-  k_update_st<<<kRedBlocks, kThreads, 0, s>>>(n, w->r, w->v, w->q, w->mv, w->s, w->t, w->sc, w->red);
-  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
-  count_launch(3);
-}
-
 static void enqueue_iteration(Matrix *m, const double *b, double *x) {
-  if (m->use_pair) return enqueue_iteration_pair(m, x);
   KrylovWork *w = m->kw;
   cudaStream_t s = m->stream;
   const int64_t n = m->n;
@@ -313,8 +261,6 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     return B200FEM_E_ZERO_DIAGONAL;
   }
   if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x, 0, n * sizeof(double), s), err);
-  const bool pair = m->use_pair = pair_wanted(m);
-  if (pair && ensure_pair_work(m)) return set_err(err, B200FEM_E_CUDA, "matvec-pair workspace allocation failed"), B200FEM_E_CUDA;
   if (launch_dot(b, b, n, &w->red, s)) return B200FEM_E_CUDA;
   double bb = 0.0;
   B200_CUDA_E(cudaMemcpyAsync(&bb, w->red.result, sizeof(double), cudaMemcpyDeviceToHost, s), err);
@@ -371,7 +317,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
       if (int rc = run_loop_graph(m, loop_graph, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
       B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
       B200_CUDA_E(cudaStreamSynchronize(s), err);
-      count_launch((pair ? 4 : 5) * (H[1].it - it0) + 1);
+      count_launch(5 * (H[1].it - it0) + 1);
       cur = 1;  // the snapshot is in H[1 + (cur ^ 1)]
     } else {
       int batch = 4;
@@ -395,10 +341,6 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     it = done.it;
     mv = done.mv;
     B200_CUDA_E(cudaGetLastError(), err);
-    if (done.status == KS_FAULT) {
-      set_err(err, B200FEM_E_CUDA, "GRID3 matvec pair: dependency wait timed out (not all CTAs resident?)");
-      return B200FEM_E_CUDA;
-    }
     if (done.status == KS_BREAKDOWN) {
       // shadow residual went orthogonal: restart from the explicit residual unless the
       // previous restart made no progress (solvers.py:144-157)
@@ -677,7 +619,6 @@ int b200fem_matrix_destroy(b200fem_matrix *mm) {
   if (!m) return 0;
   cudaStreamSynchronize(m->stream);
   free_work(m->kw);
-  if (m->pair_cnt) cudaFree(m->pair_cnt);
   cudaFree(m->chunk_node);
   delete m;
   return 0;

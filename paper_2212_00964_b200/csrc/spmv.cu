@@ -1014,238 +1014,6 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
   }
 }
 
-// ------------------------------------------------------------ GRID3 matvec pair
-// One pass over the matrix for the two matvecs of a BiCGSTAB iteration (`bicgstab` with
-// B200FEM_PAIR, krylov.cu).  With M = D^-1 A, the iteration's second operand s = r - alpha v
-// depends on a global dot (alpha), but t = M s = M r - alpha M v, so the kernel computes
-//   phase 1:  v = M p,  q = M r        (both from one read of every matrix block)
-//   phase 2:  w = M v                  (the same blocks again, lagging behind phase 1)
-// and the caller forms s = r - alpha v, t = q - alpha w once alpha is known.  Phase 2 of a
-// node needs v at its 26 lattice neighbours, written by other warps of other CTAs: phase 1
-// walks the slab-major segments (SlabWalk; each segment also computes the first row of the
-// next slab, so a segment depends only on segments of its own and the previous slab) and
-// counts finished chunk slots per segment; phase 2 of segment g waits for segments g and
-// g +- 1 of its slab and of the slab before.  Every warp runs phase 2 `lag` work items
-// behind its phase 1 (two segments + a margin): the dependencies of a phase-2 item are then
-// phase-1 items of the same or earlier loop steps, and phase 1 never waits, so with every CTA
-// resident (one per SM) the waits cannot deadlock; the matrix blocks are re-read a few MB
-// later, from L2.
-// The counters accumulate over launches (target = epoch * slots), so they are never reset
-// inside a solve.  A bounded spin sets `fault` instead of hanging.
-struct PairArgs {
-  const double *p, *r, *inv, *r0;
-  double *v, *q, *w;
-  unsigned long long *cnt;  // per segment: finished phase-1 slots, cumulative
-  unsigned long long *epoch;
-  int *fault;
-  KrylovScalars *sc;  // null: no reduction / stage
-};
-
-// Poll with a relaxed gpu-scope load (no L1 invalidation); every operand the consumer then
-// reads was produced in this launch and is loaded with ld.global.cg, i.e. from L2, the
-// coherence point the producer's release-add has made its stores visible at.
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// Row sums (A x1)_a, (A x2)_a of node a, in the order of k_spmv_grid3 (upper then lower).
-// COH: the operand is written inside this launch, so it is read with coherent loads.
-template <int NRHS, bool COH>
-__device__ __forceinline__ void grid3_node_rows(const double *__restrict__ grid, const GridDims &g, int nch, int node,
-                                                int lane, const LatticePos &p, const double *x1, const double *x2,
-                                                double (&a1)[3], double (&a2)[3]) {
-  auto ldx = [](const double *ptr) -> double {
-    if (COH) return __ldcg(ptr);
-    return __ldg(ptr);
-  };
-  const int c = node >> 5;
-  double yu1[3] = {0.0, 0.0, 0.0}, yl1[3] = {0.0, 0.0, 0.0};
-  double yu2[3] = {0.0, 0.0, 0.0}, yl2[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int qq = 0; qq < 14; ++qq) {
-    const int di = grid_di(qq), dj = grid_dj(qq), dk = grid_dk(qq);
-    const bool ok = grid_has(p, di, dj, dk);
-    const int m = node + di + dj * g.nx + dk * g.nxy;
-    const double *B = grid + ((int64_t)(qq * nch + c) * 288 + lane);
-    double b[9], xm[3], xn[3];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      xm[t] = ok ? ldx(x1 + 3 * (int64_t)m + t) : 0.0;
-      if (NRHS == 2) xn[t] = ok ? ldx(x2 + 3 * (int64_t)m + t) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      yu1[r] = fma(b[3 * r + 2], xm[2], fma(b[3 * r + 1], xm[1], fma(b[3 * r], xm[0], yu1[r])));
-      if (NRHS == 2) yu2[r] = fma(b[3 * r + 2], xn[2], fma(b[3 * r + 1], xn[1], fma(b[3 * r], xn[0], yu2[r])));
-    }
-  }
-#pragma unroll
-  for (int qq = 1; qq < 14; ++qq) {
-    const int di = grid_di(qq), dj = grid_dj(qq), dk = grid_dk(qq);
-    const bool ok = grid_has(p, -di, -dj, -dk);
-    const int m = node - di - dj * g.nx - dk * g.nxy;
-    const double *B = grid + ((int64_t)(qq * nch + (m >> 5)) * 288 + (m & 31));
-    double b[9], xm[3], xn[3];
-#pragma unroll
-    for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      xm[t] = ok ? ldx(x1 + 3 * (int64_t)m + t) : 0.0;
-      if (NRHS == 2) xn[t] = ok ? ldx(x2 + 3 * (int64_t)m + t) : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      yl1[r] = fma(b[6 + r], xm[2], fma(b[3 + r], xm[1], fma(b[r], xm[0], yl1[r])));
-      if (NRHS == 2) yl2[r] = fma(b[6 + r], xn[2], fma(b[3 + r], xn[1], fma(b[r], xn[0], yl2[r])));
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    a1[r] = yu1[r] + yl1[r];
-    a2[r] = yu2[r] + yl2[r];
-  }
-}
-
-struct PairGeom {
-  int per_seg, nk, nslab, n_seg;
-  int64_t n_work, lag;
-};
-
-__global__ void __launch_bounds__(kGThreads, kGMinBlocks)
-    k_grid3_pair(const double *__restrict__ grid, GridDims g, const uint8_t *__restrict__ dir_flag, PairGeom pg,
-                 PairArgs a, RedScratch red) {
-  if (a.sc && a.sc->status != KS_RUNNING) return;
-  const int lane = threadIdx.x & 31;
-  const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const int nch = (int)(g.npad >> 5);
-  const unsigned long long epoch = *(volatile unsigned long long *)a.epoch + 1;
-  const unsigned long long target = epoch * (unsigned long long)pg.per_seg;
-  double red0 = 0.0;
-  const int64_t n_steps = (pg.n_work + pg.lag + nwarps - 1) / nwarps;
-  for (int64_t i = 0; i < n_steps; ++i) {
-    const int64_t w1 = warp0 + i * nwarps;
-    if (w1 < pg.n_work) {  // ---- phase 1: v = M p, q = M r on segment rows + the next slab's first row
-      const int seg = (int)(w1 / pg.per_seg), slot = (int)(w1 - (int64_t)seg * pg.per_seg);
-      const int s = seg / pg.nk, k = seg - s * pg.nk;
-      const int row0 = s * g.slab, row1 = min(row0 + g.slab, g.ny), row1e = min(row1 + 1, g.ny);
-      const int lo = k * g.nxy + row0 * g.nx, own_hi = k * g.nxy + row1 * g.nx, hi = k * g.nxy + row1e * g.nx;
-      const int c = (lo >> 5) + slot, c0 = c << 5, node = c0 + lane;
-      if (c <= ((hi - 1) >> 5) && node >= lo && node < hi) {
-        const LatticePos lp = lattice_pos(node, c0, g);
-        double ap[3], ar[3];
-        grid3_node_rows<2, false>(grid, g, nch, node, lane, lp, a.p, a.r, ap, ar);
-#pragma unroll
-        for (int rr = 0; rr < 3; ++rr) {
-          const int64_t row = 3 * (int64_t)node + rr;
-          const bool d = dir_flag && __ldg(dir_flag + row);
-          const double inv = __ldg(a.inv + row);
-          const double v = inv * (d ? __ldg(a.p + row) : ap[rr]);
-          a.v[row] = v;
-          a.q[row] = inv * (d ? __ldg(a.r + row) : ar[rr]);
-          if (node < own_hi && a.sc) red0 = fma(__ldg(a.r0 + row), v, red0);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) red_release_add_u64(a.cnt + seg, 1ull);
-    }
-    const int64_t w2 = w1 - pg.lag;
-    if (w2 >= 0 && w2 < pg.n_work) {  // ---- phase 2: w = M v on the segment's own rows
-      const int seg = (int)(w2 / pg.per_seg), slot = (int)(w2 - (int64_t)seg * pg.per_seg);
-      const int s = seg / pg.nk, k = seg - s * pg.nk;
-      const int row0 = s * g.slab, row1 = min(row0 + g.slab, g.ny);
-      const int lo = k * g.nxy + row0 * g.nx, hi = k * g.nxy + row1 * g.nx;
-      const int c = (lo >> 5) + slot;
-      if (c <= ((hi - 1) >> 5)) {
-        if (lane == 0) {  // segments k-1..k+1 of this slab and of the previous one
-          for (int ds = (s > 0 ? -1 : 0); ds <= 0; ++ds)
-            for (int dk = -1; dk <= 1; ++dk) {
-              const int kk = k + dk;
-              if (kk < 0 || kk >= pg.nk) continue;
-              const unsigned long long *cp = a.cnt + (s + ds) * pg.nk + kk;
-              long long spins = 0;
-              while (ld_relaxed_u64(cp) < target) {
-                if (*(volatile int *)a.fault) break;
-                if (++spins > (1ll << 22)) {
-                  atomicExch(a.fault, 1);
-                  break;
-                }
-                __nanosleep(64);
-              }
-            }
-        }
-        __syncwarp();
-        const int c0 = c << 5, node = c0 + lane;
-        if (node >= lo && node < hi) {
-          const LatticePos lp = lattice_pos(node, c0, g);
-          double av[3], unused[3];
-          grid3_node_rows<1, true>(grid, g, nch, node, lane, lp, a.v, nullptr, av, unused);
-#pragma unroll
-          for (int rr = 0; rr < 3; ++rr) {
-            const int64_t row = 3 * (int64_t)node + rr;
-            const bool d = dir_flag && __ldg(dir_flag + row);
-            a.w[row] = __ldg(a.inv + row) * (d ? __ldcg(a.v + row) : av[rr]);
-          }
-        }
-      }
-    }
-  }
-  double v1[1] = {red0}, tot[1];
-  if (block_partials_and_finish<1, kGThreads / 32>(v1, red, tot) && threadIdx.x == 0) {
-    *(volatile unsigned long long *)a.epoch = epoch;
-    if (a.sc) {
-      if (*(volatile int *)a.fault) a.sc->status = KS_FAULT;
-      else apply_stage(ST_R0, a.sc, tot);
-    }
-  }
-}
-
-static GridDims grid_dims(const Matrix *m);
-
-bool grid3_pair_supported(const Matrix *m) {
-  return m->kind == MK_GRID3 && m->gvec == 3 && m->row_hi < 0 && m->dir_flag != nullptr;
-}
-
-int launch_grid3_pair(Matrix *m, const double *p, const double *r, const double *inv, const double *r0, double *v,
-                      double *q, double *w, KrylovScalars *sc, RedScratch *red) {
-  GridDims g = grid_dims(m);
-  if (g.slab == 0) g.slab = g.ny;  // small lattice: one slab
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  PairGeom pg{};
-  pg.nk = g.nz;
-  pg.nslab = (g.ny + g.slab - 1) / g.slab;
-  pg.n_seg = pg.nslab * pg.nk;
-  pg.per_seg = ((g.slab + 1) * g.nx + 31) / 32 + 1;
-  pg.n_work = (int64_t)pg.n_seg * pg.per_seg;
-  // phase 2 of work item w runs `lag` items after its phase 1: at least two segments (its
-  // dependencies then lie in the same or earlier loop steps of every warp -- no deadlock with
-  // all CTAs resident), plus a margin so that the waits rarely block.  The matrix blocks are
-  // re-read lag * 32 nodes * 1008 B later; that distance must stay well inside L2.
-  const char *el = getenv("B200FEM_PAIR_LAG");
-  const int extra = el ? std::max(0, atoi(el)) : 128;
-  pg.lag = 2 * (int64_t)pg.per_seg + extra;
-  if (!m->pair_cnt || m->pair_nseg < pg.n_seg) {
-    if (m->pair_cnt) cudaFree(m->pair_cnt);
-    B200_CUDA(cudaMalloc((void **)&m->pair_cnt, (pg.n_seg + 2) * sizeof(unsigned long long) + sizeof(int)));
-    B200_CUDA(cudaMemsetAsync(m->pair_cnt, 0, (pg.n_seg + 2) * sizeof(unsigned long long) + sizeof(int), m->stream));
-    m->pair_nseg = pg.n_seg;
-  }
-  PairArgs a{p, r, inv, r0, v, q, w, m->pair_cnt, m->pair_cnt + pg.n_seg, (int *)(m->pair_cnt + pg.n_seg + 1), sc};
-  RedScratch rs = red ? *red : RedScratch{};
-  k_grid3_pair<<<sms, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, pg, a, rs);
-  count_launch();
-  return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
-}
-
 // Scalar (vec 1, Poisson) GRID: one value per offset; a thread per node, 4 CTAs per SM.
 template <int MODE>
 __global__ void __launch_bounds__(kGThreads, 4) k_spmv_grid1(const double *__restrict__ grid, GridDims g,
