@@ -223,3 +223,38 @@ def test_incremental_zero_schedule(aluminum):
     hist = incremental_solve(LinearElasticityProblem(mesh, aluminum, specs), LoadSchedule((0.0, 0.0, 0.0)))
     for rec in hist.steps:
         assert np.abs(rec.U).max() == 0.0
+
+
+def test_criterion_9_solver_scale_and_determinism(aluminum):
+    """test_acceptance.py:302-339 (>= 100k-DOF elastic solve under budget; the reference's
+    thread-count bit-identity becomes run-to-run bit-identity of R, K and dU on the device).
+    The reference publishes 15 s single-threaded for this solve (pkg/test_output.txt:222)."""
+    import time
+
+    import torch
+    t0 = time.perf_counter()
+    mesh = generate_box_mesh(32, 32, 32, 1, 1, 1)
+    specs = zero_dirichlet(BoundaryLocator.plane(2, 0.0)) + [
+        DirichletSpec(BoundaryLocator.plane(2, 1.0), 2, lambda p: 0.01)]
+    prob = LinearElasticityProblem(mesh, aluminum, specs)
+    n = prob.n_dofs
+    assert n >= 100_000
+
+    def solve():
+        U0 = np.zeros(n)
+        R = assemble_residual(prob, U0)
+        K = assemble_jacobian(prob, U0)
+        dU = fem.bicgstab_jacobi(K, -R, cfg=fem.LinearSolveConfig(rel_tol=1e-10, abs_tol=1e-14))
+        return R, K, dU
+
+    R, K, dU = solve()
+    torch.cuda.synchronize()
+    first = time.perf_counter() - t0  # includes mesh, workspace (pattern) and library start-up
+    rel = np.linalg.norm(K @ dU + R) / np.linalg.norm(R)
+    t1 = time.perf_counter()
+    R2, K2, dU2 = solve()
+    torch.cuda.synchronize()
+    warm = time.perf_counter() - t1
+    assert rel <= 1e-10 and first < 300
+    assert np.array_equal(R, R2) and np.array_equal(K.data, K2.data) and np.array_equal(dU, dU2)
+    print(f"criterion 9: {n} DOF, rel residual {rel:.2e}, first call {first:.2f} s, warm {warm * 1e3:.1f} ms")
