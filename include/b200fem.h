@@ -247,6 +247,18 @@ int b200fem_gather_sum(const double *x_dev, const int64_t *idx_dev, int64_t n, d
 int b200fem_axpy(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
 int b200fem_scale(int64_t n, double a, const double *x_dev, double *y_dev, void *stream);
 
+/* ---- the reference's low seam (gradfem.kernels, kernels.py:1-55; SURVEY 8(b) seam 1),
+ * bit-identical to its numba kernels (same accumulation order, no FMA contraction).
+ * csr_matvec: replaces kernels.csr_matvec (kernels.py:37-47, numba body 21-28): y = A x,
+ * per row sequential in storage order.  int32 indptr/indices as the reference's CsrMatrix.
+ * scatter_add: replaces kernels.scatter_add (kernels.py:50-55, numba body 30-34):
+ * values[dest[k]] += contribs[k] in ascending k, in place; B200FEM_E_INVALID if a dest is
+ * outside [0, n_values). */
+int b200fem_csr_matvec_seq(int64_t n_rows, const int32_t *indptr_dev, const int32_t *indices_dev,
+                           const double *data_dev, const double *x_dev, double *y_dev, void *stream);
+int b200fem_scatter_add(double *values_dev, int64_t n_values, const int64_t *dest_dev, const double *contribs_dev,
+                        int64_t n, void *stream, b200fem_error *err);
+
 /* ---- host output formatting.  Rows of a (rows, cols) array as text lines,
  * values space-separated, "%.17g" for doubles (= Python f"{x:.17g}", the reference's
  * io_vtk._fmt, io_vtk.py:18-19), "%lld" for integers with an optional leading `prefix`

@@ -119,6 +119,8 @@ SIGNATURES = {
     "b200fem_format_i64_rows": (C.c_int64, [_vp, _i64, C.c_int32, _i64, _vp, _i64]),
     "b200fem_gather_sum": (C.c_int, [_vp, _vp, _i64, _pf64, _vp]),
     "b200fem_axpy": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
+    "b200fem_csr_matvec_seq": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "b200fem_scatter_add": (C.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, C.POINTER(Error)]),
     "b200fem_scale": (C.c_int, [_i64, _f64, _vp, _vp, _vp]),
 }
 
