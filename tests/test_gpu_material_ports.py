@@ -129,3 +129,107 @@ def test_j2_path_dependence_against_scalar_oracle(aluminum):
         assert np.allclose(sig, c_dev * dev0 + press * np.eye(3), atol=1e-10)
         prob.commit(U)
     assert np.abs(sig).max() > 1.0  # residual stress after unloading to zero strain
+
+
+def test_linear_elastic_symmetric_output(rng):
+    """test_materials.py:52-56 (25 random grad u in [-0.05, 0.05])"""
+    c = fem.ElasticConstants(E=70e3, nu=0.3)
+    for _ in range(25):
+        sig = device_flux(fem.LinearElasticityProblem, c, rng.uniform(-0.05, 0.05, (3, 3)))[0]
+        assert np.abs(sig - sig.T).max() <= 1e-12 * max(1.0, np.abs(sig).max())
+
+
+def test_linear_elastic_tangent_constant(rng):
+    """test_materials.py:59-67 (the device tangent of LE does not depend on the state)"""
+    c = fem.ElasticConstants(E=70e3, nu=0.3)
+    mesh = fem.generate_box_mesh(2, 1, 1, 2.0, 1.0, 1.0)
+    prob = fem.LinearElasticityProblem(mesh, c, [])
+    Ks = [fem.assemble_jacobian(prob, 0.01 * rng.standard_normal(prob.n_dofs)).data for _ in range(3)]
+    assert np.allclose(Ks[0], Ks[1], rtol=1e-12, atol=0) and np.allclose(Ks[1], Ks[2], rtol=1e-12, atol=0)
+
+
+def neo_hookean_energy(F, c):  # W = G/2 (J^(-2/3) tr(F^T F) - 3) + kappa/2 (J - 1)^2 (materials.py:80-84)
+    J = np.linalg.det(F)
+    return 0.5 * c.G * (J ** (-2.0 / 3.0) * np.trace(F.T @ F) - 3.0) + 0.5 * c.kappa * (J - 1.0) ** 2
+
+
+def test_neo_hookean_matches_fd_of_energy(aluminum, rng):
+    """test_materials.py:90-103: the device flux against central differences of the energy"""
+    gu = 1e-3 * rng.standard_normal((3, 3))
+    P = device_flux(fem.NeoHookeanProblem, aluminum, gu)[0]
+    h = 1e-6
+    F = gu + np.eye(3)
+    P_fd = np.zeros((3, 3))
+    for i in range(3):
+        for j in range(3):
+            d = np.zeros((3, 3))
+            d[i, j] = h
+            P_fd[i, j] = (neo_hookean_energy(F + d, aluminum) - neo_hookean_energy(F - d, aluminum)) / (2 * h)
+    assert np.abs(P - P_fd).max() / np.abs(P_fd).max() < 1e-6
+
+
+def test_neo_hookean_objectivity(aluminum, rng):
+    """test_materials.py:114-120 states it on the energy, W(QF) = W(F); the device evaluates
+    the flux, for which it reads P(QF) = Q P(F) (10 random rotations)."""
+    from scipy.spatial.transform import Rotation
+
+    F = np.eye(3) + 0.05 * rng.standard_normal((3, 3))
+    P0 = device_flux(fem.NeoHookeanProblem, aluminum, F - np.eye(3))[0]
+    for q in Rotation.random(10, rng).as_matrix():
+        Pq = device_flux(fem.NeoHookeanProblem, aluminum, q @ F - np.eye(3))[0]
+        assert np.allclose(Pq, q @ P0, rtol=1e-10, atol=1e-10 * np.abs(P0).max())
+
+
+def test_j2_tangent_finite_at_zero_deviator(aluminum):
+    """test_materials.py:193-196: the consistent tangent at a zero deviator (pure dilation and
+    the reference state) is finite"""
+    mesh = fem.generate_box_mesh(1, 1, 1, 1.0, 1.0, 1.0)
+    prob = fem.J2PlasticityProblem(mesh, aluminum, [])
+    for G in (np.zeros((3, 3)), 0.01 * np.eye(3)):
+        U = (mesh.nodes @ G.T).ravel()
+        assert np.all(np.isfinite(fem.assemble_jacobian(prob, U).data))
+        assert np.all(np.isfinite(fem.assemble_residual(prob, U)))
+
+
+def test_j2_at_exact_yield_uses_elastic_branch():
+    """test_materials.py:199-211: at f == 0 exactly (yield stress = the device's own trial
+    s_eff) the return map keeps the elastic branch: flux and tangent equal the elastic ones"""
+    base = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=1.0)
+    gu = 0.003 * np.diag([1.0, 0.0, 0.0])
+    sig_tr = device_flux(fem.LinearElasticityProblem, base, gu)[0]
+    s = sig_tr - np.trace(sig_tr) / 3.0 * np.eye(3)
+    c = fem.ElasticConstants(E=70e3, nu=0.3, sigma_yield=float(np.sqrt(1.5 * (s * s).sum())))
+    out, pj, U = device_flux(fem.J2PlasticityProblem, c, gu)
+    ref, pl, _ = device_flux(fem.LinearElasticityProblem, c, gu)
+    assert np.allclose(out, ref, rtol=1e-14, atol=0)
+    assert np.allclose(fem.assemble_jacobian(pj, U).data, fem.assemble_jacobian(pl, U).data, rtol=1e-13, atol=1e-9)
+
+
+def test_commit_state(aluminum, rng):
+    """test_materials.py:214-228, through J2PlasticityProblem.commit on the device"""
+    mesh = fem.generate_box_mesh(1, 1, 1, 1.0, 1.0, 1.0)
+    prob = fem.J2PlasticityProblem(mesh, aluminum, [])
+    prob.commit(np.zeros(prob.n_dofs))
+    st = prob.state
+    assert np.array_equal(st.eps_prev, np.zeros_like(st.eps_prev))
+    assert np.array_equal(st.sig_prev, np.zeros_like(st.sig_prev))
+    gu = 1e-5 * rng.standard_normal((3, 3))  # elastic range
+    U = (mesh.nodes @ gu.T).ravel()
+    prob.commit(U)
+    st1 = prob.state
+    sig_le = device_flux(fem.LinearElasticityProblem, aluminum, gu)[0]
+    assert np.allclose(st1.sig_prev, np.broadcast_to(sig_le, st1.sig_prev.shape), atol=1e-12)
+    prob.commit(U)  # zero increment is a fixed point
+    st2 = prob.state
+    assert np.array_equal(st2.eps_prev, st1.eps_prev) and np.array_equal(st2.sig_prev, st1.sig_prev)
+
+
+def test_flux_zero_for_all_models(aluminum):
+    """test_materials.py:231-239"""
+    z = np.zeros((3, 3))
+    assert np.abs(device_flux(fem.LinearElasticityProblem, aluminum, z)[0]).max() == 0.0
+    assert np.abs(device_flux(fem.NeoHookeanProblem, aluminum, z)[0]).max() < 1e-10
+    assert np.abs(device_flux(fem.J2PlasticityProblem, aluminum, z)[0]).max() == 0.0
+    mesh = fem.generate_box_mesh(1, 1, 1, 1.0, 1.0, 1.0)
+    pois = fem.PoissonProblem(mesh, 2.0, [])
+    assert np.abs(fem.quad_point_stress(pois, np.zeros(pois.n_dofs))).max() == 0.0
