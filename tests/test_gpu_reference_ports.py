@@ -258,3 +258,65 @@ def test_criterion_9_solver_scale_and_determinism(aluminum):
     assert rel <= 1e-10 and first < 300
     assert np.array_equal(R, R2) and np.array_equal(K.data, K2.data) and np.array_equal(dU, dU2)
     print(f"criterion 9: {n} DOF, rel residual {rel:.2e}, first call {first:.2f} s, warm {warm * 1e3:.1f} ms")
+
+
+def test_param_vjp_zero_covector():
+    """test_assembly.py:203-207"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    prob = PoissonProblem(mesh, 1.0, [], design_source=True)
+    out = fem.assemble_param_vjp(prob, np.zeros(prob.n_dofs), prob.theta, np.zeros(prob.n_dofs))
+    assert np.array_equal(out, np.zeros(mesh.n_nodes))
+
+
+def test_param_vjp_matches_dense_fd(rng):
+    """test_assembly.py:210-234 (device VJP against central differences of the device residual)"""
+    mesh = generate_box_mesh(2, 2, 2, 1, 1, 1)
+    prob = PoissonProblem(mesh, 1.0, [DirichletSpec(onbox_locator(1, 1, 1), 0, lambda p: 0.0)], design_source=True)
+    theta = rng.standard_normal(mesh.n_nodes)
+    prob.set_theta(theta)
+    U = rng.standard_normal(prob.n_dofs) * 0.1
+    w = rng.standard_normal(prob.n_dofs)
+    got = fem.assemble_param_vjp(prob, U, theta, w)
+    ws = workspace(prob)
+    w_eff = w.copy()
+    w_eff[ws.dir_dofs] = 0.0
+    h = 1e-6
+    expect = np.zeros(mesh.n_nodes)
+    for m in range(mesh.n_nodes):
+        e = np.zeros(mesh.n_nodes)
+        e[m] = h
+        prob.set_theta(theta + e)
+        Rp = assemble_residual(prob, U)
+        prob.set_theta(theta - e)
+        Rm = assemble_residual(prob, U)
+        expect[m] = w_eff @ (Rp - Rm) / (2 * h)
+    prob.set_theta(theta)
+    assert np.abs(got - expect).max() / np.abs(expect).max() < 1e-6
+
+
+def test_param_vjp_element_locality(aluminum, rng):
+    """test_assembly.py:237-256"""
+    mesh = generate_box_mesh(3, 1, 1, 3, 1, 1)
+    prob = fem.SimpElasticityProblem(mesh, fem.LinearElastic(aluminum), zero_dirichlet(BoundaryLocator.plane(0, 0.0)))
+    prob.set_theta(rng.uniform(0.4, 0.9, mesh.n_cells))
+    U = 0.01 * rng.standard_normal(prob.n_dofs)
+    ws = workspace(prob)
+    w = np.zeros(prob.n_dofs)
+    w[ws.edofs[1]] = rng.standard_normal(24)
+    got = fem.assemble_param_vjp(prob, U, prob.theta, w)
+    assert got[1] != 0.0
+    w2 = np.zeros(prob.n_dofs)
+    w2[np.setdiff1d(ws.edofs[2], ws.edofs[1])] = 1.0
+    assert fem.assemble_param_vjp(prob, U, prob.theta, w2)[0] == 0.0
+
+
+def test_param_vjp_simp_penalization_derivative(aluminum, rng):
+    """test_assembly.py:259-269: theta = 1, p = 3 -> three times the unpenalised residual"""
+    mesh = generate_box_mesh(1, 1, 1, 1, 1, 1)
+    prob = fem.SimpElasticityProblem(mesh, fem.LinearElastic(aluminum), dirichlet=[])
+    prob.set_theta(np.ones(1))
+    U = 0.01 * rng.standard_normal(prob.n_dofs)
+    w = rng.standard_normal(prob.n_dofs)
+    R_lin = assemble_residual(prob, U)
+    vjp = fem.assemble_param_vjp(prob, U, prob.theta, w)
+    assert np.isclose(vjp[0], 3.0 * (w @ R_lin), rtol=1e-12)
