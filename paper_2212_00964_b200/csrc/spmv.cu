@@ -1066,11 +1066,15 @@ static GridDims grid_dims(const Matrix *m) {
   GridDims g{};
   g.nx = m->gnx, g.ny = m->gny, g.nz = m->gnz, g.nxy = m->gnx * m->gny, g.nn = (int)(m->n / m->gvec), g.npad = m->gnpad;
   g.slab = 0;
-  if (m->gvec == 3) {  // slabs of ~4096 nodes per plane, once the plane is larger than 4 slabs
+  if (m->gvec == 3) {  // slabs of ~4096 nodes per plane, once a plane of blocks outgrows L2 reuse
     const char *e = getenv("B200FEM_GRID_SLAB");  // per launch: tests switch it in-process
     const int env = e ? atoi(e) : -1;
+    // plain order while one plane of blocks (nxy * 1008 B) stays under ~24 MB: its lower-block
+    // re-reads still hit L2 there (ncu: +3 % DRAM at 136^3, a plane of 19 MB), and the order
+    // of the fused Krylov dots -- hence the rounding of every iterate -- stays the plain one
     const int rows = env >= 0 ? env : (4096 + g.nx - 1) / g.nx;
-    if (rows > 0 && (env >= 0 || g.ny >= 4 * rows)) g.slab = std::min(rows, g.ny);
+    const bool big_plane = (int64_t)g.nxy * 1008 > (int64_t)24 << 20;
+    if (rows > 0 && (env >= 0 || (big_plane && g.ny >= 4 * rows))) g.slab = std::min(rows, g.ny);
   }
   return g;
 }
