@@ -30,12 +30,13 @@ def main():
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--method", default="bicgstab")
     ap.add_argument("--material", default="nh")
+    ap.add_argument("--operator", default="grid", choices=["csr", "grid"], help="grid: the Newton operator")
     a = ap.parse_args()
     prob = problem(a.n, a.material)
     ws = fem.workspace(prob)
     N = prob.n_dofs
     U = D.zeros(N)
-    K = fem.assemble_jacobian(prob, U)
+    K = fem.solvers._tangent_matrix(prob, U, a.operator)
     R = D.empty(N)
     ws.residual(prob, U, R)
     b = -R
