@@ -164,6 +164,15 @@ int b200fem_matrix_fem_grid(b200fem_matrix **out, b200fem_ctx *ctx, const double
  * adjoint's lambda_d = b_d - (K^T x)_d with x_d = 0 (adjoint.py:25-31, PCG split) */
 #define B200FEM_GRID_PRE_DIRICHLET 1
 int b200fem_matrix_fem_grid_ex(b200fem_matrix **out, b200fem_ctx *ctx, const double *grid_dev, int32_t flags);
+/* Opt-in mixed-precision Newton operator (LinearSolveConfig(operator="grid32")): the GRID3
+ * matvec streams a single-precision copy of the values (half the bytes), with FP64 operands,
+ * products, sums and Krylov vectors; the diagonal (Jacobi) stays FP64.  An inexact-Newton
+ * variant of the K handed to bicgstab_jacobi by newton_solve (solvers.py:218): the residual
+ * and the Newton stopping test are unchanged FP64.  grid_to_f32 rounds the n values to nearest
+ * (same layout);
+ * set_f32(m, NULL) restores the FP64 values (GRID3, vec 3 only). */
+int b200fem_grid_to_f32(const double *grid_dev, float *grid32_dev, int64_t n_values, void *stream);
+int b200fem_matrix_set_f32(b200fem_matrix *m, const float *data32_dev);
 /* generic CSR on the device (any square matrix with sorted unique columns) */
 int b200fem_matrix_csr(b200fem_matrix **out, int64_t n, int64_t nnz, const int32_t *indptr_dev,
                        const int32_t *indices_dev, const double *data_dev, void *stream);

@@ -89,6 +89,8 @@ SIGNATURES = {
     "b200fem_matrix_fem_grid": (C.c_int, [C.POINTER(_vp), _vp, _vp]),
     "b200fem_matrix_fem_grid_ex": (C.c_int, [C.POINTER(_vp), _vp, _vp, C.c_int32]),
     "b200fem_matrix_set_data": (C.c_int, [_vp, _vp]),
+    "b200fem_grid_to_f32": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
+    "b200fem_matrix_set_f32": (C.c_int, [_vp, _vp]),
     "b200fem_matrix_destroy": (C.c_int, [_vp]),
     "b200fem_matvec": (C.c_int, [_vp, _vp, _vp]),
     "b200fem_diagonal": (C.c_int, [_vp, _vp]),

@@ -165,6 +165,7 @@ struct Matrix {
   // GRID3: lattice nodes per axis and the padded offset-array length (data = 14 arrays)
   int gnx = 0, gny = 0, gnz = 0, gvec = 3;
   int64_t gnpad = 0;
+  const float *data32 = nullptr;  // GRID3 vec 3: single-precision copy used by the matvec
 };
 
 // ------------------------------------------------------------------ GRID3 offsets

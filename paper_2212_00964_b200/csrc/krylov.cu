@@ -577,6 +577,28 @@ int b200fem_matrix_fem_grid_ex(b200fem_matrix **out, b200fem_ctx *ctx, const dou
   return 0;
 }
 
+// FP64 GRID3 values -> their FP32 copy (same layout), rounded to nearest
+__global__ void k_grid_to_f32(const double *__restrict__ a, float *__restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __double2float_rn(a[i]);
+}
+
+int b200fem_grid_to_f32(const double *src, float *dst, int64_t n, void *stream) {
+  if (n < 0 || n % 288 || (n && (!src || !dst))) return B200FEM_E_INVALID;
+  if (!n) return 0;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads));
+  k_grid_to_f32<<<g, kThreads, 0, (cudaStream_t)stream>>>(src, dst, n);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
+}
+
+int b200fem_matrix_set_f32(b200fem_matrix *mat, const float *data32) {
+  Matrix *m = (Matrix *)mat;
+  if (!m || m->kind != MK_GRID3 || m->gvec != 3) return B200FEM_E_INVALID;
+  m->data32 = data32;
+  return 0;
+}
+
 int b200fem_ctx_grid_size(const b200fem_ctx *ctx, int64_t *n_values, int32_t *dims) {
   const Ctx *c = (const Ctx *)ctx;
   if (!c || !n_values) return B200FEM_E_INVALID;

@@ -870,6 +870,10 @@ int prepare_sym3_chunks(Matrix *m) {
 // Dirichlet rows give y = x (identity rows).  Summation order is fixed -> deterministic.
 constexpr int kGThreads = 256;
 constexpr int kGMinBlocks = 1;  // 255 registers: ILP per thread beats more warps (2/SM: +41 %)
+#ifndef GRID32_MIN_BLOCKS
+#define GRID32_MIN_BLOCKS 2
+#endif
+constexpr int kGMinBlocks32 = GRID32_MIN_BLOCKS;  // FP32 copy: 2 CTAs/SM at 128 registers, 328 us vs 389 us at 1 (3: 333 us)
 
 struct GridDims {
   int nx, ny, nz, nxy, nn;  // nodes per axis, per plane, total
@@ -939,8 +943,27 @@ __device__ __forceinline__ SlabWalk slab_walk(const GridDims &g, int node_lo, in
   return sw;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const double *__restrict__ grid, GridDims g,
+// A lattice block's 9 values (value e at +32 e) in FP64, or in the FP32 copy written by
+// b200fem_grid_to_f32.  `tile` = (offset, 32-node tile).
+__device__ __forceinline__ void grid_block(const double *__restrict__ grid, int64_t tile, int lane, bool ok,
+                                           double (&b)[9]) {
+  const double *B = grid + tile * 288 + lane;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // normal L2 policy (see below)
+}
+__device__ __forceinline__ void grid_block(const float *__restrict__ grid, int64_t tile, int lane, bool ok,
+                                           double (&b)[9]) {
+  // same layout in FP32.  Tried: two float4 + one float per lane (3 loads instead of 9):
+  // 690-717 us against 391 us for these scalar loads at config 3
+  const float *B = grid + tile * 288 + lane;
+#pragma unroll
+  for (int e = 0; e < 9; ++e) b[e] = ok ? (double)__ldg(B + 32 * e) : 0.0;
+}
+
+// VT = double: the stored tangent.  VT = float: its single-precision copy (opt-in
+// operator "grid32", b200fem_matrix_set_f32): half the value bytes, products and sums in FP64.
+template <int MODE, typename VT>
+__global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : kGMinBlocks) k_spmv_grid3(const VT *__restrict__ grid, GridDims g,
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
                                                              int node_hi, SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
@@ -973,10 +996,8 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, di, dj, dk);
       const int m = node + di + dj * g.nx + dk * g.nxy;
-      const double *B = grid + ((int64_t)(q * nch + c) * 288 + lane);
       double b[9], xm[3];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // first use: normal L2 policy
+      grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
@@ -991,10 +1012,8 @@ __global__ void __launch_bounds__(kGThreads, kGMinBlocks) k_spmv_grid3(const dou
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, -di, -dj, -dk);
       const int m = node - di - dj * g.nx - dk * g.nxy;
-      const double *B = grid + ((int64_t)(q * nch + (m >> 5)) * 288 + (m & 31));
       double b[9], xm[3];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // normal policy (see below)
+      grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);  // normal policy (see below)
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
@@ -1143,7 +1162,11 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
       k_spmv_grid1<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
     } else {
       const int gg = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (nch + 7) / 8));
-      k_spmv_grid3<MODE><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
+      if (m->data32)
+        k_spmv_grid3<MODE, float><<<(int)std::min<int64_t>((int64_t)kGMinBlocks32 * gg, std::max(1, (nch + 7) / 8)),
+                                    kGThreads, 0, m->stream>>>(m->data32, g, m->dir_flag, lo, hi, a, r);
+      else
+        k_spmv_grid3<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
     }
   } else if (m->kind == MK_FEM3 && m->use_tma && m->n_chunks > 0) {  // chunks cover the row range
     int dev = 0, sms = 148;

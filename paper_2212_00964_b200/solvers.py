@@ -42,6 +42,9 @@ class LinearSolveConfig:
     #           lower blocks re-read from L2 as contiguous slices; csrc/spmv.cu);
     #  "sym"  = symmetric node-block storage for any vec-3 mesh (L2-gather bound: 1.64 ms vs
     #           0.85 ms per config-3 matvec, profiles/)
+    #  "grid32" = opt-in inexact Newton: GRID3 with the values rounded to FP32 (half the
+    #           bytes; FP64 vectors, products and sums; FP64 residual and Newton test), for
+    #           vec-3 box lattices only.  NOT the reference's FP64 operator.
     operator: str = "auto"
 
     def __post_init__(self):
@@ -49,7 +52,7 @@ class LinearSolveConfig:
             raise ValueError("linear solver tolerances must be positive")
         if self.method not in ("bicgstab", "pcg"):
             raise ValueError(f"unknown linear solver {self.method!r}")
-        if self.operator not in ("auto", "grid", "sym", "csr"):
+        if self.operator not in ("auto", "grid", "sym", "csr", "grid32"):
             raise ValueError(f"unknown operator {self.operator!r}")
 
 
@@ -154,6 +157,16 @@ class NewtonReport:
 def _tangent_matrix(problem, U, operator="csr"):
     """K at U; cached for jacobian_constant problems (solvers.py:177-184)."""
     ws = workspace(problem)
+    if operator == "grid32":
+        if not (ws.has_grid and problem.vec == 3):
+            raise ValueError('operator "grid32" needs a vec-3 box-lattice problem')
+        K = ws._cache.get("newton_grid32")
+        if K is None:
+            K = GridOperator(ws)
+            ws._cache["newton_grid32"] = K
+        ws.jacobian_grid(problem, U, K.device_data)
+        K.refresh_f32()
+        return K
     if operator in ("auto", "grid") and ws.has_grid:
         if problem.jacobian_constant:
             K = getattr(problem, "_jac_cache", None)

@@ -236,6 +236,17 @@ class GridOperator(_NodeBlockOperator):
     _ctor = "b200fem_matrix_fem_grid"
     _size = "grid_size"
 
+    def refresh_f32(self):
+        """Round the current values into the single-precision copy that the matvec then streams
+        (operator "grid32", b200fem_matrix_set_f32); call after every re-assembly."""
+        lib = _lib.lib()
+        if getattr(self, "device_data32", None) is None:
+            self.device_data32 = D.empty(self.device_data.numel(), D.torch().float32)
+            raise_for(lib.b200fem_matrix_set_f32(self._device_handle(), D.ptr(self.device_data32)), None,
+                      "matrix_set_f32")
+        raise_for(lib.b200fem_grid_to_f32(D.ptr(self.device_data), D.ptr(self.device_data32), self.device_data.numel(),
+                                     D.stream()), None, "grid_to_f32")
+
     def matvec_pre_dirichlet(self, x):
         """K0 x: the same values without the identity Dirichlet rows (device in, device out)."""
         h = getattr(self, "_raw", None)

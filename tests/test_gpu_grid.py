@@ -139,3 +139,43 @@ def test_newton_grid_scalar_matches_csr(method):
     from paper_2212_00964_b200.sparse import GridOperator
     assert isinstance(p2._jac_cache, GridOperator)
     assert r1.n_iterations == r2.n_iterations and rel(U2, U1) < 1e-9
+
+
+# ------------------------------------------- opt-in inexact Newton: FP32-stored GRID3 values
+def test_grid32_matvec_rounds_only_the_values(rng):
+    """operator "grid32": the matvec of the FP32 copy equals the FP64 operator to the FP32
+    rounding of the values (FP64 products and sums), and the identity rows stay exact."""
+    _, prob, U = build("nh_block", dict(CASES["nh_block"], dims=(12, 7, 9)))
+    U = (U if U is not None else np.zeros(prob.n_dofs)) + 1e-3 * rng.standard_normal(prob.n_dofs)
+    G = grid_of(prob, U)
+    x = rng.standard_normal(prob.n_dofs)
+    y64 = G @ x
+    vals = G.device_data.cpu().numpy()
+    G.refresh_f32()
+    assert np.array_equal(G.device_data32.cpu().numpy(), vals.astype(np.float32))
+    y32 = G @ x
+    assert 0.0 < rel(y32, y64) < 1e-6
+    dd = fem.workspace(prob).dir_dofs
+    assert np.array_equal(y32[dd], x[dd])
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "pcg"])
+def test_newton_grid32_reaches_the_fp64_solution(method):
+    """Inexact Newton with the FP32-stored tangent converges to the FP64 Newton solution
+    (FP64 residual and stopping test): U within the north_star bar of 1e-8."""
+    dims = (9, 8, 12)
+    _, p1, _ = build("nh_block", dict(CASES["nh_block"], dims=dims))
+    _, p2, _ = build("nh_block", dict(CASES["nh_block"], dims=dims))
+    kw = dict(cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11))
+    U1, r1 = fem.newton_solve(p1, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method,
+                                                               operator="grid"), **kw)
+    U2, r2 = fem.newton_solve(p2, lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-14, method=method,
+                                                               operator="grid32"), **kw)
+    assert r2.converged and r2.n_iterations <= r1.n_iterations + 1
+    assert rel(U2, U1) < 1e-8
+
+
+def test_grid32_rejects_scalar_and_non_lattice_problems():
+    _, prob, _ = build("poisson")
+    with pytest.raises(ValueError, match="grid32"):
+        fem.newton_solve(prob, lin_cfg=fem.LinearSolveConfig(operator="grid32"))
