@@ -952,12 +952,13 @@ __device__ __forceinline__ void grid_block(const double *__restrict__ grid, int6
   for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0;  // normal L2 policy (see below)
 }
 __device__ __forceinline__ void grid_block(const float *__restrict__ grid, int64_t tile, int lane, bool ok,
-                                           double (&b)[9]) {
-  // same layout in FP32.  Tried: two float4 + one float per lane (3 loads instead of 9):
-  // 690-717 us against 391 us for these scalar loads at config 3
+                                           float (&b)[9]) {
+  // same layout in FP32, kept in FP32 registers until the FP64 FMA that uses it.  Tried: two
+  // float4 + one float per lane (3 loads instead of 9): 690-717 us against 391 us for these
+  // scalar loads at config 3 (one CTA per SM)
   const float *B = grid + tile * 288 + lane;
 #pragma unroll
-  for (int e = 0; e < 9; ++e) b[e] = ok ? (double)__ldg(B + 32 * e) : 0.0;
+  for (int e = 0; e < 9; ++e) b[e] = ok ? __ldg(B + 32 * e) : 0.0f;
 }
 
 // VT = double: the stored tangent.  VT = float: its single-precision copy (opt-in
@@ -996,12 +997,14 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, di, dj, dk);
       const int m = node + di + dj * g.nx + dk * g.nxy;
-      double b[9], xm[3];
+      VT b[9];
+      double xm[3];
       grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) yu[r] = fma(b[3 * r + 2], xm[2], fma(b[3 * r + 1], xm[1], fma(b[3 * r], xm[0], yu[r])));
+      for (int r = 0; r < 3; ++r)
+        yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
     }
 #pragma unroll
     // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
@@ -1012,12 +1015,14 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
       const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
       const bool ok = grid_has(p, -di, -dj, -dk);
       const int m = node - di - dj * g.nx - dk * g.nxy;
-      double b[9], xm[3];
+      VT b[9];
+      double xm[3];
       grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);  // normal policy (see below)
 #pragma unroll
       for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) yl[r] = fma(b[6 + r], xm[2], fma(b[3 + r], xm[1], fma(b[r], xm[0], yl[r])));
+      for (int r = 0; r < 3; ++r)
+        yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
     }
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
