@@ -80,15 +80,14 @@ int b200fem_stream_sync(void *stream);
  * coords_host (n_nodes,3) f64, cells_host (n_cells,8) int64 in VTK HEX8 order.
  * Builds on the device: the geometry check (map_elements, elements.py:117-131),
  * the node adjacency / CSR pattern / scatter positions (sparse.py:75-108),
- * diagonal slots (assembly.py:96-97) and the cell colouring used for the
- * deterministic reduction. */
+ * diagonal slots (assembly.py:96-97) and the node -> cell lists of the ordered
+ * (ascending cell id, kernels.py:30-34) per-node gathers. */
 int b200fem_ctx_create(b200fem_ctx **out, int64_t n_nodes, int64_t n_cells, int32_t vec,
                        const double *coords_host, const int64_t *cells_host, int32_t material,
                        const double *params /* [8] */, int32_t flags, void *stream,
                        b200fem_error *err);
 int b200fem_ctx_destroy(b200fem_ctx *ctx);
-int b200fem_ctx_info(const b200fem_ctx *ctx, int64_t *n_dofs, int64_t *nnz, int32_t *n_colors,
-                     int32_t *max_neighbors);
+int b200fem_ctx_info(const b200fem_ctx *ctx, int64_t *n_dofs, int64_t *nnz, int32_t *max_neighbors);
 
 /* pattern copy-outs for bit-exact parity checks (device outputs, caller-sized) */
 int b200fem_copy_indptr(b200fem_ctx *ctx, int32_t *indptr_dev /* n_dofs+1 */);
@@ -109,7 +108,8 @@ int b200fem_set_state(b200fem_ctx *ctx, const double *eps_prev, const double *si
 int b200fem_get_state(b200fem_ctx *ctx, double *eps_prev_dev, double *sig_prev_dev);
 
 /* ---- assembly (assembly.py:236-261, 273-300) ----
- * residual: R = sum_e R_e(U) (deterministic colour-ordered reduction)
+ * residual: R = sum_e R_e(U) (per-node gather in ascending cell id: the reference's
+ *           sequential scatter order, kernels.py:30-34; no atomics)
  *           - bc_scale*f_neumann - f_body; Dirichlet rows -> U[d]-bc_scale*u_D.
  * norm_host (nullable) receives ||R||_2 (forces a stream sync).            */
 int b200fem_residual(b200fem_ctx *ctx, const double *U_dev, double bc_scale,
@@ -124,6 +124,27 @@ int b200fem_volume_average_flux(b200fem_ctx *ctx, const double *U_dev, double *o
                                 b200fem_error *err);
 /* J2 state commit eps <- sym grad u, sig <- return map (problems.py:155-163) */
 int b200fem_commit_state(b200fem_ctx *ctx, const double *U_dev);
+/* geometry of every cell (map_elements, elements.py:80-131; Workspace.phys_grads / JxW,
+ * assembly.py:64-80): phys_grads (N_e,8q,8i,3), JxW (N_e,8q); either output nullable */
+int b200fem_geometry(b200fem_ctx *ctx, double *phys_grads_dev, double *jxw_dev);
+
+/* ---- constitutive laws over a batch of points (materials.py:74-194) ----
+ * No context needed: material_id B200FEM_MAT_*, params[8] as for ctx_create (host).
+ * grad_u (n, vec, 3) dev.  J2: eps_prev, sig_prev (n,3,3) dev (the committed state).
+ * Outputs (dev, nullable): flux (n, vec, 3) = linear_elastic_flux / neo_hookean_flux /
+ * j2_return_map / alpha grad u; tangent (n, 3vec, 3vec) = d flux / d grad u (the hand
+ * tangent the element kernels use); eps_out, sig_out (J2, both or
+ * neither) = commit_state (materials.py:125-131); det_f (n) = det F (NH; 1 otherwise).
+ * NH points with det F <= 0 get zero flux / tangent and the call returns
+ * B200FEM_E_INVERTED_DEFORMATION (err->cell = first such point, err->value = min det F;
+ * materials.py:94-100).  Synchronises `stream`. */
+int b200fem_law_batch(int32_t material_id, const double *params, int64_t n, const double *grad_u_dev,
+                      const double *eps_prev_dev, const double *sig_prev_dev, double *flux_dev,
+                      double *tangent_dev, double *eps_out_dev, double *sig_out_dev, double *det_f_dev,
+                      void *stream, b200fem_error *err);
+/* neo_hookean_energy(F) (materials.py:80-85) for F (n,3,3) dev -> W (n) dev; params[2] = G,
+ * params[3] = kappa.  Asynchronous on `stream`. */
+int b200fem_nh_energy_batch(const double *params, int64_t n, const double *F_dev, double *W_dev, void *stream);
 
 /* ---- adjoint half ---- */
 /* param_vjp: out = w_eff^T dR/dtheta at U (assembly.py:303-341); w_eff zeroes the Dirichlet

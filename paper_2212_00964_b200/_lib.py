@@ -61,7 +61,7 @@ SIGNATURES = {
     "b200fem_stream_sync": (C.c_int, [_vp]),
     "b200fem_ctx_create": (C.c_int, [C.POINTER(_vp), _i64, _i64, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _perr]),
     "b200fem_ctx_destroy": (C.c_int, [_vp]),
-    "b200fem_ctx_info": (C.c_int, [_vp, _pi64, _pi64, _pi32, _pi32]),
+    "b200fem_ctx_info": (C.c_int, [_vp, _pi64, _pi64, _pi32]),
     "b200fem_copy_indptr": (C.c_int, [_vp, _vp]),
     "b200fem_copy_indices": (C.c_int, [_vp, _vp]),
     "b200fem_copy_dest": (C.c_int, [_vp, _i64, _i64, _vp]),
@@ -76,6 +76,9 @@ SIGNATURES = {
     "b200fem_qp_flux": (C.c_int, [_vp, _vp, _vp, _perr]),
     "b200fem_volume_average_flux": (C.c_int, [_vp, _vp, _vp, _perr]),
     "b200fem_commit_state": (C.c_int, [_vp, _vp]),
+    "b200fem_geometry": (C.c_int, [_vp, _vp, _vp]),
+    "b200fem_law_batch": (C.c_int, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _perr]),
+    "b200fem_nh_energy_batch": (C.c_int, [_vp, _i64, _vp, _vp, _vp]),
     "b200fem_param_vjp": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _perr]),
     "b200fem_transpose_fem": (C.c_int, [_vp, _vp, _vp]),
     "b200fem_csr_transpose": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

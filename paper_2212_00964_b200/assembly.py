@@ -2,7 +2,7 @@
 
 ``workspace(problem)`` replaces the reference's host cache (assembly.py:83-145) with a
 device context (csrc/context.cu): geometry check, CSR pattern, scatter positions,
-diagonal slots and the cell colouring are built on the B200; the Dirichlet table and the
+diagonal slots and the node -> cell lists of the ordered gathers are built on the B200; the Dirichlet table and the
 fixed Neumann / body load vectors are computed here on the host once (north_star: host
 code keeps the Dirichlet handling) and uploaded.
 
@@ -172,9 +172,9 @@ class DeviceWorkspace:
                                     self._stream, C.byref(err))
         raise_for(st, err, "ctx_create")
         self.ctx = ctx
-        n_dofs, nnz, ncol, mx = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
-        lib.b200fem_ctx_info(ctx, C.byref(n_dofs), C.byref(nnz), C.byref(ncol), C.byref(mx))
-        self.n_dofs, self.nnz, self.n_colors, self.max_neighbors = n_dofs.value, nnz.value, ncol.value, mx.value
+        n_dofs, nnz, mx = C.c_int64(), C.c_int64(), C.c_int32()
+        lib.b200fem_ctx_info(ctx, C.byref(n_dofs), C.byref(nnz), C.byref(mx))
+        self.n_dofs, self.nnz, self.max_neighbors = n_dofs.value, nnz.value, mx.value
         dd = np.ascontiguousarray(self.dir_dofs, dtype=np.int64)
         dv = np.ascontiguousarray(self.dir_values, dtype=np.float64)
         raise_for(lib.b200fem_set_dirichlet(ctx, D.hptr(dd), D.hptr(dv), dd.size), None, "set_dirichlet")
@@ -182,7 +182,7 @@ class DeviceWorkspace:
         fb = self.f_body if np.any(self.f_body) else None
         raise_for(lib.b200fem_set_loads(ctx, D.hptr(fn) if fn is not None else None,
                                         D.hptr(fb) if fb is not None else None), None, "set_loads")
-        self._theta_key = None
+        self._theta_host = None  # copy of the theta last uploaded (content-keyed sync)
         if isinstance(problem, J2PlasticityProblem):
             self.upload_state(problem._host_state)
         self._cache = {}
@@ -197,17 +197,24 @@ class DeviceWorkspace:
 
     # ------------------------------------------------------------ syncing
     def sync(self, problem):
+        """Mirror the host-side mutable inputs the reference re-reads at every assembly
+        (problems.py:76-93 theta, 150-157 J2 state): theta is compared by CONTENT with the copy
+        last uploaded (in-place edits and attribute reassignment both count; O(n_design) host
+        compare), and a live host view of the J2 state is re-uploaded."""
+        sv = getattr(problem, "_state_view", None)
+        if sv is not None:
+            self.upload_state(sv)
         if problem.design_layout is None:
             return
         if problem.theta is None:
             raise ValueError("problem has a design layout but no theta bound")
-        key = (id(problem.theta), problem._theta_version)
-        if key != self._theta_key:
-            th = np.ascontiguousarray(problem.theta, dtype=np.float64)
-            if th.shape != (problem.n_design,):
-                raise ValueError(f"theta must have shape ({problem.n_design},), got {th.shape}")
+        th = np.asarray(problem.theta, dtype=np.float64)
+        if th.shape != (problem.n_design,):
+            raise ValueError(f"theta must have shape ({problem.n_design},), got {th.shape}")
+        if self._theta_host is None or not np.array_equal(th, self._theta_host):
+            th = np.array(th, dtype=np.float64, order="C", copy=True)
             raise_for(_lib.lib().b200fem_set_theta(self.ctx, D.hptr(th), th.size, 1), None, "set_theta")
-            self._theta_key = key
+            self._theta_host = th
 
     def upload_state(self, st: QuadPointState):
         eps = np.ascontiguousarray(st.eps_prev, dtype=np.float64)
@@ -341,6 +348,33 @@ class DeviceWorkspace:
     @property
     def dest(self) -> np.ndarray:
         return self._cached("dest", lambda: self.dest_slice(0, self.n_cells).astype(np.int64))
+
+    def _geometry(self):
+        pg = D.empty(self.n_cells * 8 * 8 * 3)
+        jxw = D.empty(self.n_cells * 8)
+        raise_for(_lib.lib().b200fem_geometry(self.ctx, D.ptr(pg), D.ptr(jxw)), None, "geometry")
+        return D.to_host(pg).reshape(self.n_cells, 8, 8, 3), D.to_host(jxw).reshape(self.n_cells, 8)
+
+    @property
+    def phys_grads(self) -> np.ndarray:
+        """(N_e, 8q, 8i, 3) physical shape-function gradients (Workspace.phys_grads, assembly.py:64-80;
+        map_elements, elements.py:117-131), computed on the device on first access (the kernels
+        recompute them per cell instead of streaming 1.5 KB/cell)."""
+        if "geometry" not in self._cache:
+            self._cache["geometry"] = self._geometry()
+        return self._cache["geometry"][0]
+
+    @property
+    def JxW(self) -> np.ndarray:
+        """(N_e, 8q) det J times the Gauss weights (all 1) (Workspace.JxW)."""
+        if "geometry" not in self._cache:
+            self._cache["geometry"] = self._geometry()
+        return self._cache["geometry"][1]
+
+    @property
+    def shape_values(self) -> np.ndarray:
+        """(8q, 8i) shape functions at the Gauss points (Workspace.shape_values)."""
+        return shape_values_at_gauss()
 
     @property
     def edofs(self) -> np.ndarray:

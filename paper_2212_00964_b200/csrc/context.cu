@@ -1,4 +1,4 @@
-// Context lifecycle, CSR pattern / scatter-position build, colouring, boundary data,
+// Context lifecycle, CSR pattern / scatter-position build, boundary data,
 // and the small deterministic vector reductions.
 //
 // Reference being replaced: assembly.workspace() (assembly.py:83-145) and
@@ -242,34 +242,9 @@ static int grid_for(int64_t n, int threads = kThreads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
-// greedy colouring in cell order: a cell takes the lowest colour unused by any cell
-// sharing one of its nodes.  Colour classes are node-disjoint -> race-free scatter.
-static int color_cells_host(const int64_t *cells, int64_t n_cells, int64_t n_nodes, std::vector<int32_t> &order,
-                            std::vector<int64_t> &off) {
-  std::vector<uint64_t> used(n_nodes, 0);
-  std::vector<uint8_t> col(n_cells);
-  int ncol = 0;
-  for (int64_t e = 0; e < n_cells; ++e) {
-    uint64_t u = 0;
-    for (int k = 0; k < 8; ++k) u |= used[cells[e * 8 + k]];
-    if (~u == 0) return -1;
-    int c = __builtin_ctzll(~u);
-    col[e] = (uint8_t)c;
-    ncol = std::max(ncol, c + 1);
-    for (int k = 0; k < 8; ++k) used[cells[e * 8 + k]] |= (1ull << c);
-  }
-  off.assign(ncol + 1, 0);
-  for (int64_t e = 0; e < n_cells; ++e) off[col[e] + 1]++;
-  for (int c = 0; c < ncol; ++c) off[c + 1] += off[c];
-  std::vector<int64_t> cur(off.begin(), off.end() - 1);
-  order.resize(n_cells);
-  for (int64_t e = 0; e < n_cells; ++e) order[cur[col[e]]++] = (int32_t)e;
-  return ncol;
-}
-
 static void free_ctx(Ctx *c) {
   if (!c) return;
-  void *ptrs[] = {c->coords, c->cells, c->nbr_ptr, c->nbr, c->indptr, c->cpos, c->diag, c->color_cells,
+  void *ptrs[] = {c->coords, c->cells, c->nbr_ptr, c->nbr, c->indptr, c->cpos, c->diag,
                   c->dir_dofs, c->dir_vals, c->f_neumann, c->f_body, c->theta, c->eps_prev, c->sig_prev, c->derr,
                   c->n2c_ptr, c->n2c, c->n2c_a, c->dir_flag, c->scratch, c->up_ptr, c->lo_blk};
   for (void *p : ptrs) cudaFree(p);
@@ -458,17 +433,6 @@ static int build(Ctx *c, const double *coords_h, const int64_t *cells_h, b200fem
 
   detect_grid(c, cells_h);
 
-  // ---- colouring
-  std::vector<int32_t> order;
-  int ncol = color_cells_host(cells_h, ne, nn, order, c->color_off);
-  if (ncol < 0) {
-    cleanup();
-    set_err(err, B200FEM_E_UNSUPPORTED, "cell colouring needs more than 64 colours");
-    return B200FEM_E_UNSUPPORTED;
-  }
-  c->n_colors = ncol;
-  B200_CUDA_E(dalloc(&c->color_cells, ne), err);
-  B200_CUDA_E(cudaMemcpyAsync(c->color_cells, order.data(), ne * sizeof(int32_t), cudaMemcpyHostToDevice, s), err);
   B200_CUDA_E(cudaStreamSynchronize(s), err);
   cleanup();
   B200_CUDA_E(cudaGetLastError(), err);
@@ -594,12 +558,11 @@ int b200fem_ctx_destroy(b200fem_ctx *ctx) {
   return 0;
 }
 
-int b200fem_ctx_info(const b200fem_ctx *ctx, int64_t *n_dofs, int64_t *nnz, int32_t *n_colors, int32_t *max_nbr) {
+int b200fem_ctx_info(const b200fem_ctx *ctx, int64_t *n_dofs, int64_t *nnz, int32_t *max_nbr) {
   const Ctx *c = (const Ctx *)ctx;
   if (!c) return B200FEM_E_INVALID;
   if (n_dofs) *n_dofs = c->n_dofs;
   if (nnz) *nnz = c->nnz;
-  if (n_colors) *n_colors = c->n_colors;
   if (max_nbr) *max_nbr = c->max_nbr;
   return 0;
 }

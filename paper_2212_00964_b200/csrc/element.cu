@@ -6,15 +6,17 @@
 //   materials.py:74-131  linear_elastic_flux, neo_hookean_flux (AD of W), j2_return_map
 //   problems.py:166-202  SIMP theta^p scaling;  problems.py:319-324 nodal design source
 //   assembly.py:176-300  _element_residual, assemble_residual, assemble_jacobian
-//   kernels.py:30-34     sequential scatter_add -> colour-ordered deterministic RMW
+//   kernels.py:30-34     sequential scatter_add -> ordered per-node gathers
 //
-// Reduction: cells are processed colour by colour (colour classes share no node), so
-// every R entry / CSR slot is updated by plain read-modify-write with no atomics and a
-// fixed order (colour 0 first) -> results are bit-identical from run to run.
+// Reduction: per-cell blocks go to a scratch buffer; a per-node gather (or, on box lattices,
+// the lattice pull) then sums every R entry / CSR slot over its cells in ascending cell id --
+// the reference's sequential scatter order -- with no atomics, so results are bit-identical
+// from run to run.
 
 #include <cmath>
 
 #include "internal.cuh"
+#include "laws.cuh"
 
 namespace b200 {
 
@@ -97,25 +99,6 @@ __device__ __forceinline__ double qp_geometry(const double (*X)[3], int q, doubl
   return det;
 }
 
-__device__ __forceinline__ double det3(const double (&F)[3][3]) {  // autodiff.py:202-206 expansion
-  return F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) - F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
-         F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
-}
-
-// H = F^{-T} = cof(F) / J
-__device__ __forceinline__ void inv_transpose(const double (&F)[3][3], double J, double (&H)[3][3]) {
-  const double r = 1.0 / J;
-  H[0][0] = (F[1][1] * F[2][2] - F[1][2] * F[2][1]) * r;
-  H[0][1] = (F[1][2] * F[2][0] - F[1][0] * F[2][2]) * r;
-  H[0][2] = (F[1][0] * F[2][1] - F[1][1] * F[2][0]) * r;
-  H[1][0] = (F[0][2] * F[2][1] - F[0][1] * F[2][2]) * r;
-  H[1][1] = (F[0][0] * F[2][2] - F[0][2] * F[2][0]) * r;
-  H[1][2] = (F[0][1] * F[2][0] - F[0][0] * F[2][1]) * r;
-  H[2][0] = (F[0][1] * F[1][2] - F[0][2] * F[1][1]) * r;
-  H[2][1] = (F[0][2] * F[1][0] - F[0][0] * F[1][2]) * r;
-  H[2][2] = (F[0][0] * F[1][1] - F[0][1] * F[1][0]) * r;
-}
-
 struct ElemArgs {
   const double *coords;
   const int32_t *cells;
@@ -125,112 +108,6 @@ struct ElemArgs {
   MatParams mp;
   DevErr *derr;
 };
-
-// J2 trial state (materials.py:104-122): returns sig_trial, deviator s, s_eff (guarded),
-// and whether ssq > 0.
-__device__ __forceinline__ void j2_trial(const double (&gu)[3][3], const double *ep, const double *sp,
-                                         const MatParams &mp, double (&st)[3][3], double (&s)[3][3], double &seff,
-                                         bool &pos) {
-  double de[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) de[i][j] = 0.5 * (gu[i][j] + gu[j][i]) - ep[i * 3 + j];
-  const double tr = de[0][0] + de[1][1] + de[2][2];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) st[i][j] = sp[i * 3 + j] + ((i == j) ? mp.lam * tr : 0.0) + 2.0 * mp.mu * de[i][j];
-  const double p = (st[0][0] + st[1][1] + st[2][2]) / 3.0;
-  double ss = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      s[i][j] = st[i][j] - (i == j ? p : 0.0);
-      ss += s[i][j] * s[i][j];
-    }
-  const double ssq = 1.5 * ss;
-  pos = ssq > 0.0;
-  seff = sqrt(pos ? ssq : 1.0);
-}
-
-// flux P (vec x 3) at one quadrature point; returns false on det F <= 0 (NH)
-template <int MAT>
-__device__ __forceinline__ bool flux_at(const double (&gu)[3][3], const MatParams &mp, const double *ep,
-                                        const double *sp, double (&P)[3][3], double &detF) {
-  if (MAT == B200FEM_MAT_POISSON) {
-#pragma unroll
-    for (int d = 0; d < 3; ++d) P[0][d] = mp.alpha * gu[0][d];
-    return true;
-  } else if (MAT == B200FEM_MAT_LE) {
-    const double tr = gu[0][0] + gu[1][1] + gu[2][2];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) P[i][j] = (i == j ? mp.lam * tr : 0.0) + mp.mu * (gu[i][j] + gu[j][i]);
-    return true;
-  } else if (MAT == B200FEM_MAT_NH) {
-    // P = G J^{-2/3} (F - I1/3 H) + kappa (J-1) J H  (tests/test_materials.py:71-77 closed
-    // form of the reference's AD of W), rewritten in terms of g = grad u so that no O(1)
-    // quantities cancel near F = I:
-    //   J - 1 = I1(g) + I2(g) + I3(g),  cof F = I + c,  c = tr(g) I - g^T + cof(g)
-    //   F - I1/3 H = [ (Jm1 - e) I + (1 + Jm1) g - (1 + e) c ] / J,  e = (2 tr g + |g|^2)/3
-    //   kappa (J-1) J H = kappa Jm1 cof F
-    const double trg = gu[0][0] + gu[1][1] + gu[2][2];
-    double cg[3][3];  // cofactor matrix of g
-    cg[0][0] = gu[1][1] * gu[2][2] - gu[1][2] * gu[2][1];
-    cg[0][1] = gu[1][2] * gu[2][0] - gu[1][0] * gu[2][2];
-    cg[0][2] = gu[1][0] * gu[2][1] - gu[1][1] * gu[2][0];
-    cg[1][0] = gu[0][2] * gu[2][1] - gu[0][1] * gu[2][2];
-    cg[1][1] = gu[0][0] * gu[2][2] - gu[0][2] * gu[2][0];
-    cg[1][2] = gu[0][1] * gu[2][0] - gu[0][0] * gu[2][1];
-    cg[2][0] = gu[0][1] * gu[1][2] - gu[0][2] * gu[1][1];
-    cg[2][1] = gu[0][2] * gu[1][0] - gu[0][0] * gu[1][2];
-    cg[2][2] = gu[0][0] * gu[1][1] - gu[0][1] * gu[1][0];
-    const double I2 = cg[0][0] + cg[1][1] + cg[2][2];
-    const double I3 = gu[0][0] * cg[0][0] + gu[0][1] * cg[0][1] + gu[0][2] * cg[0][2];
-    const double Jm1 = trg + I2 + I3;
-    const double J = 1.0 + Jm1;
-    detF = J;
-    if (!(J > 0.0)) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) P[i][j] = 0.0;
-      return false;
-    }
-    double gg = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) gg += gu[i][j] * gu[i][j];
-    const double e = (2.0 * trg + gg) / 3.0;
-    const double dI = (Jm1 - e);
-    const double rc = rcbrt(J);
-    const double Ga = mp.mu * (rc * rc) / J;  // G J^{-2/3} / J (rcbrt: far cheaper than pow)
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double c = (i == j ? trg : 0.0) - gu[j][i] + cg[i][j];
-        const double dev = (i == j ? dI : 0.0) + (1.0 + Jm1) * gu[i][j] - (1.0 + e) * c;
-        P[i][j] = Ga * dev + mp.kappa * Jm1 * ((i == j ? 1.0 : 0.0) + c);
-      }
-    return true;
-  } else {  // J2 perfect plasticity, radial return
-    double st[3][3], s[3][3], seff;
-    bool pos;
-    j2_trial(gu, ep, sp, mp, st, s, seff, pos);
-    const double over = fmax(seff - mp.sy, 0.0);
-    const double f = over / seff;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) P[i][j] = st[i][j] - s[i][j] * f;
-    return true;
-  }
-}
 
 // 8-lane reduce-scatter: lane q of the group ends with the sum over the group of v[q*V..]
 template <int V>
@@ -673,16 +550,27 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
 #pragma unroll
         for (int d = 0; d < 3; ++d) S.g[q][k][d] = Gk[t][d];
       }
-      bool bad_def = false, fin = true;
+      bool bad_def = false, fin = true, vfin = true;
       double detF = 1.0;
       if (MAT == B200FEM_MAT_POISSON) {
         if (part == 0) S.coef[q][0] = a.mp.alpha * scale;
+        // the flux value alpha grad u must be finite (the reference checks the AD value first,
+        // assembly.py:216-233, even though this tangent does not depend on U)
+        double gs = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gs += fabs(quad_sum(S.U[part][0] * Gk[0][d] + S.U[part + 4][0] * Gk[1][d]));
+        vfin = isfinite(gs);
       } else {
         double gu[3][3];
+        double gs = 0.0;
 #pragma unroll
         for (int v = 0; v < 3; ++v)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) gu[v][d] = quad_sum(S.U[part][v] * Gk[0][d] + S.U[part + 4][v] * Gk[1][d]);
+          for (int d = 0; d < 3; ++d) {
+            gu[v][d] = quad_sum(S.U[part][v] * Gk[0][d] + S.U[part + 4][v] * Gk[1][d]);
+            gs += fabs(gu[v][d]);
+          }
+        vfin = isfinite(gs);
         if (MAT == B200FEM_MAT_LE) {
           if (part == 0) {
             S.coef[q][0] = a.mp.mu * scale;
@@ -698,7 +586,7 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
           const double J = det3(F);
           detF = J;
           double H[3][3];
-          if (J > 0.0) {
+          if (!(J <= 0.0)) {  // NaN: a non-finite value, not an inversion (materials.py:94)
             inv_transpose(F, J, H);
           } else {
             bad_def = true;
@@ -712,6 +600,7 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) I1 += F[i][j] * F[i][j];
+          vfin = vfin && isfinite(J) && isfinite(I1);
           const double rc = bad_def ? 0.0 : rcbrt(J);
           const double aa = rc * rc;  // J^{-2/3}
           const double Ga = a.mp.mu * aa;
@@ -747,6 +636,7 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
           const double c1 = (a.mp.mu - 0.5 * beta) * scale, cl = (a.mp.lam + beta / 3.0) * scale;
           const double c3 = -gam * scale;
           fin = isfinite(c1) && isfinite(cl) && isfinite(c3);
+          vfin = vfin && isfinite(seff) && isfinite(st[0][0] + st[1][1] + st[2][2]);
           if (part == 0) {
             S.coef[q][0] = c1;
             S.coef[q][1] = cl;
@@ -769,6 +659,8 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
         if (bad_def) {
           atomicMin(&a.derr->inv_def, key);
           atomicMin(&a.derr->min_detF, ord_bits(detF));
+        } else if (!vfin) {  // the flux value itself is non-finite (assembly.py:228-233)
+          atomicMin(&a.derr->nonfin_v, key);
         } else if (!fin) {
           atomicMin(&a.derr->nonfin_d, key);
         }
@@ -993,6 +885,33 @@ __global__ void __launch_bounds__(kThreads) k_qp(ElemArgs a, int64_t n_cells, do
   if (MODE == 2) {
     double tot[10];
     block_partials_and_finish<10>(acc, red, tot);
+  }
+}
+
+// ------------------------------------------------- geometry (Workspace fields)
+// thread per (cell, qp): phys_grads[e][q][k][:] = J^-T dphi_k, JxW[e][q] = det J (weights 1;
+// elements.py:80-131).  Host views only (the kernels recompute geometry per cell).
+__global__ void __launch_bounds__(kThreads) k_geometry(const double *__restrict__ coords,
+                                                        const int32_t *__restrict__ cells, int64_t n_cells,
+                                                        double *__restrict__ pg, double *__restrict__ jxw) {
+  const int64_t total = n_cells * 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t >> 3;
+    const int q = t & 7;
+    double X[8][3];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) X[k][d] = coords[(int64_t)cells[e * 8 + k] * 3 + d];
+    double G[8][3];
+    const double det = qp_geometry(X, q, G);
+    if (jxw) jxw[t] = det;
+    if (pg) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) pg[(t * 8 + k) * 3 + d] = G[k][d];
+    }
   }
 }
 
@@ -1477,5 +1396,15 @@ int b200fem_volume_average_flux(b200fem_ctx *ctx, const double *U, double *out_h
 }
 
 int b200fem_commit_state(b200fem_ctx *ctx, const double *U) { return launch_commit((Ctx *)ctx, U); }
+
+int b200fem_geometry(b200fem_ctx *ctx, double *phys_grads, double *jxw) {
+  Ctx *c = (Ctx *)ctx;
+  if (!c) return B200FEM_E_INVALID;
+  if (c->n_cells == 0 || (!phys_grads && !jxw)) return 0;
+  k_geometry<<<grid_cap(c->n_cells * 8, kThreads), kThreads, 0, c->stream>>>(c->coords, c->cells, c->n_cells,
+                                                                            phys_grads, jxw);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : B200FEM_E_CUDA;
+}
 
 }  // extern "C"

@@ -109,10 +109,6 @@ struct Ctx {
   uint8_t *dir_flag = nullptr;  // (n_dofs) 1 on Dirichlet rows
   double *scratch = nullptr;    // per-cell element blocks (two-phase assembly)
   size_t scratch_len = 0;
-  // colouring (host offsets, device cell lists ordered by colour then cell id)
-  int n_colors = 0;
-  std::vector<int64_t> color_off;
-  int32_t *color_cells = nullptr;
   // boundary data
   int64_t n_dir = 0;
   int32_t *dir_dofs = nullptr;

@@ -173,7 +173,7 @@ def subproblem(problem, plan: PartPlan):
         sub.theta = np.asarray(problem.theta)[plan.local_nodes]
         sub._theta_version = 0
     if hasattr(problem, "_host_state"):
-        st = problem.state
+        st = problem._current_state()
         sub._host_state = QuadPointState(st.eps_prev[plan.local_cells], st.sig_prev[plan.local_cells])
     return sub
 

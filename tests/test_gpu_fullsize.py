@@ -1,5 +1,9 @@
-"""Config 3 at its full size (136^3 cells, 7,714,059 DOF), where the reference itself cannot be
-run (~65 GB and hours on the CPU): size-independent properties instead.
+"""Config 3 at its full size (136^3 cells, 7,714,059 DOF): SELF-CONSISTENCY checks of the device
+path (GPU against GPU), where the reference package cannot run in the 62 GB build container
+(~65 GB and hours on the CPU).  The comparison against a reference-algorithm
+solve at this size is the oracle-port run on the GPU box's host (tools/cpu_reference.py
+port136, profiles/r02_port136.json); C2/C4/C5 against the reference package are in
+test_gpu_fullsize_ref.py.
 
 * the GRID3 operator and the reference-layout CSR operator are the same linear map;
 * Newton through three different linear paths -- BiCGSTAB on GRID3 (the bench path), PCG on
@@ -52,7 +56,7 @@ def test_fullsize_grid_operator_equals_csr():
     ws.jacobian_grid(prob, U, G.device_data)
     x = D.to_device(np.random.default_rng(0).standard_normal(prob.n_dofs))
     yk, yg = D.to_host(K.matvec(x)), D.to_host(G.matvec(x))
-    assert rel(yg, yk) < 1e-14
+    assert rel(yg, yk) < 1e-14, "self-consistency: GRID3 operator != CSR operator"
 
 
 def test_fullsize_newton_paths_agree(solutions):
@@ -60,26 +64,8 @@ def test_fullsize_newton_paths_agree(solutions):
     U0, r0 = out["grid_bicgstab"]
     for key in ("grid_pcg", "csr_bicgstab"):
         U, r = out[key]
-        assert r.converged and r.n_iterations == r0.n_iterations == 3
-        assert rel(U, U0) < 1e-8, key
+        assert r.converged and r.n_iterations == r0.n_iterations == 3, f"self-consistency ({key}): Newton count"
+        assert rel(U, U0) < 1e-8, f"self-consistency: {key} U differs from grid_bicgstab U"
     norms = r0.residual_norms
     assert norms[-1] <= 1e-10 * norms[0]
     assert norms[3] < norms[2] ** 1.5  # quadratic convergence at the end
-
-
-def test_config2_poisson_matches_reference_values():
-    """BASELINE config 2 at full size (100^3 cells, 1.03M DOF): the reference's BiCGSTAB run
-    gives max u = 5.622140e-02 after 200 matvecs."""
-    mesh = fem.generate_box_mesh(100, 100, 100, 1.0, 1.0, 1.0)
-    onb = fem.BoundaryLocator(lambda p: (np.abs(np.asarray(p) - 0.5) >= 0.5 - 1e-9).any(axis=-1))
-    out = {}
-    for method in ("bicgstab", "pcg"):
-        prob = fem.PoissonProblem(mesh, 1.0, [fem.DirichletSpec(onb, 0, lambda p: 0.0)],
-                                  source=lambda p: np.ones(np.asarray(p).shape[:-1] + (1,)))
-        U, rep = fem.newton_solve(prob, lin_cfg=fem.LinearSolveConfig(method=method))
-        out[method] = (U, rep)
-    U, rep = out["bicgstab"]
-    assert abs(U.max() - 5.622140e-02) <= 5e-9  # the reference's 7 significant digits
-    mv = sum(s.matvecs for s in rep.linear_stats)
-    assert 180 <= mv <= 220  # reference: 200 (round-off moves Krylov counts by a few %)
-    assert rel(out["pcg"][0], U) < 1e-8
