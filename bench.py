@@ -48,7 +48,24 @@ def parse():
     p.add_argument("--no-alt", action="store_true", help="skip the one-solve measurement of the other method")
     p.add_argument("--partitioned", action="store_true",
                    help="use the partitioned (multi-GPU) solver even on one rank (path check)")
+    p.add_argument("--spawn", action="store_true",
+                   help="launch the ranks through torch.distributed.run even for --gpus 1 (spawn-path check)")
     return p.parse_args()
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one
+    process per GPU, NCCL), exactly as the driver's torchrun command does, and pass rank 0's
+    JSON line through.  Returns the exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    argv = [a for a in sys.argv[1:] if a != "--spawn"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def config(n, stretch):
@@ -287,6 +304,9 @@ def run_ours(args):
     rep = reports[-1]
     lin_iters = [s_.iterations for s_ in rep.linear_stats]
     matvecs = sum(s_.matvecs for s_ in rep.linear_stats)
+    lin_s = (getattr(rep, "timings", None) or {}).get("linear_s")
+    # one Krylov iteration inside the timed solve (restart residuals included), device time
+    in_solve_iter_ms = (lin_s / max(sum(lin_iters), 1) * 1e3) if lin_s else None
 
     # ---------------- kernel-level evidence (after the timed region, same stream, CUDA events)
     if part is None:
@@ -430,7 +450,7 @@ def run_ours(args):
         "newton": {"linear_method": args.linear, "iterations": rep.n_iterations,
                    "phase_s": getattr(rep, "timings", None),
                    "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
-                   "per_step_ms": per_step},
+                   "in_solve_iter_ms": in_solve_iter_ms, "per_step_ms": per_step},
         "alt_linear": alt,
         "alt_mixed_precision": mixed,
         "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": n_cells_l / t_res / 1e6,
@@ -486,4 +506,6 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    if "WORLD_SIZE" not in os.environ and (a.gpus > 1 or a.spawn):
+        sys.exit(spawn_ranks(a))
     run_reference(a) if a.impl == "reference" else run_ours(a)

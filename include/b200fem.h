@@ -234,10 +234,17 @@ int b200fem_part_create(b200fem_part **out, b200fem_matrix *local, int64_t own_n
                         const int32_t *recv_nodes_host);
 int b200fem_part_destroy(b200fem_part *part);
 /* BiCGSTAB over all parts (solvers.py:87-167 semantics, global tolerances and counters);
- * b[p], x[p] are the parts' local device vectors (owned entries are the unknowns). */
+ * b[p], x[p] are the parts' local device vectors (owned entries are the unknowns).  Batches of
+ * iterations run as one captured CUDA graph (kernels + NCCL halo / allreduce) when the parts
+ * share a stream; B200FEM_NO_GRAPH=1 enqueues them eagerly. */
 int b200fem_dist_bicgstab(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *b,
                           double *const *x, int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters,
                           b200fem_solve_info *info, b200fem_error *err);
+/* Jacobi-PCG over all parts (b200fem_pcg semantics: x_d = b_d on Dirichlet rows, symmetric
+ * operator; one halo and two allreduces per iteration). */
+int b200fem_dist_pcg(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *b,
+                     double *const *x, int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters,
+                     b200fem_solve_info *info, b200fem_error *err);
 /* ghost entries of vec[p] <- owners' values */
 int b200fem_dist_halo(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *vec);
 /* sum over parts of the owned-range dot products */

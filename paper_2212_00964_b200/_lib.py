@@ -108,6 +108,8 @@ SIGNATURES = {
     "b200fem_part_destroy": (C.c_int, [_vp]),
     "b200fem_dist_bicgstab": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo),
                                         _perr]),
+    "b200fem_dist_pcg": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo),
+                                   _perr]),
     "b200fem_dist_halo": (C.c_int, [_vp, _i32, _vp, _vp]),
     "b200fem_dist_dot": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _pf64]),
     "b200fem_norm2": (C.c_int, [_vp, _i64, _pf64, _vp]),

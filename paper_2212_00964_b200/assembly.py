@@ -12,6 +12,7 @@ host arrays for host inputs (drop-in); pass a CUDA tensor U to stay on the devic
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 from typing import Callable
@@ -194,6 +195,26 @@ class DeviceWorkspace:
                 _lib._lib.b200fem_ctx_destroy(ctx)
             except Exception:
                 pass
+
+    @contextlib.contextmanager
+    def on_stream(self):
+        """Make the context's stream torch's current stream for the block: every launch, torch
+        allocation and copy of a multi-call sequence (the Newton loop) then shares one stream
+        with the library's kernels.  When the caller's stream differs it is joined both ways
+        (the context waits for the caller's pending work, the caller for the block's); yields
+        the caller's stream in that case, else None."""
+        t = D.torch()
+        cur = t.cuda.current_stream()
+        if cur.cuda_stream == (self._stream.value or 0):
+            yield None
+            return
+        ext = t.cuda.ExternalStream(self._stream.value or 0)
+        ext.wait_stream(cur)
+        try:
+            with t.cuda.stream(ext):
+                yield cur
+        finally:
+            cur.wait_stream(ext)
 
     # ------------------------------------------------------------ syncing
     def sync(self, problem):

@@ -251,6 +251,15 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
                             RedScratch red, int inline_stage);
 int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol,
              int64_t max_iters, b200fem_solve_info *info, b200fem_error *err);
+__global__ void k_begin_cg(KrylovScalars *S);
+__global__ void k_set_dirichlet(double *__restrict__ x, const double *__restrict__ b, const int32_t *__restrict__ d,
+                                int64_t n);
+__global__ void __launch_bounds__(kThreads) k_cg_update_xrz(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                                                            const double *__restrict__ p, const double *__restrict__ q,
+                                                            const double *__restrict__ inv, double *__restrict__ z,
+                                                            KrylovScalars *S, RedScratch red, int inline_stage);
+__global__ void __launch_bounds__(kThreads) k_cg_update_p(int64_t n, const double *__restrict__ z,
+                                                          double *__restrict__ p, const KrylovScalars *S);
 
 // ------------------------------------------------------ Krylov scalar stages
 // BiCGSTAB iteration start (solvers.py:131-139): it += 1, rho_new = r0.r, breakdown test, beta.

@@ -5,7 +5,9 @@
 //   * a halo of the SpMV operand (p, then s): owned values of interface nodes -> the ghost
 //     entries of the neighbouring parts (packed, ncclSend/ncclRecv),
 //   * three FP64 sum-allreduces of the fused dot groups {r0.v}, {t.t, t.s},
-//     {||D r||^2, r0.r, r.r}, after which every part applies the same scalar update.
+//     {||D r||^2, r0.r, r.r}, after which every part applies the same scalar update
+//     (Jacobi-PCG: one halo and two allreduces, {p.Ap}, {r.r, r.z}).
+// Batches of iterations run as one CUDA graph with the NCCL calls captured (run_batches).
 // Communicators: NCCL across processes (one part per process and GPU), or "local": all
 // parts in one process on one device, exchanged by device copies and summed by a kernel
 // in part order -- the same algorithm, used to verify partitioning on a single B200.
@@ -221,7 +223,7 @@ struct Dist {
   }
 };
 
-static void enqueue_dist_iteration(Dist &D, double *const *x) {
+static int enqueue_dist_iteration(Dist &D, double *const *x) {
   const size_t np = D.parts.size();
   std::vector<double *> pv(np), sv(np);
   for (size_t p = 0; p < np; ++p) {
@@ -239,8 +241,8 @@ static void enqueue_dist_iteration(Dist &D, double *const *x) {
     a1[p] = SpmvArgs{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
     a2[p] = SpmvArgs{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
   }
-  D.spmv(SP_JACOBI_R0, a1, pv.data(), 1);
-  D.allreduce(1);
+  int st = D.spmv(SP_JACOBI_R0, a1, pv.data(), 1);
+  st |= D.allreduce(1);
   D.stage(ST_R0);
   for (size_t p = 0; p < np; ++p) {
     Part *P = D.parts[p];
@@ -249,8 +251,8 @@ static void enqueue_dist_iteration(Dist &D, double *const *x) {
     k_update_s<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->s + lo, w->sc);
     count_launch();
   }
-  D.spmv(SP_JACOBI_TT, a2, sv.data(), 2);
-  D.allreduce(2);
+  st |= D.spmv(SP_JACOBI_TT, a2, sv.data(), 2);
+  st |= D.allreduce(2);
   D.stage(ST_TT);
   for (size_t p = 0; p < np; ++p) {
     Part *P = D.parts[p];
@@ -260,13 +262,133 @@ static void enqueue_dist_iteration(Dist &D, double *const *x) {
                                                          w->r0 + lo, w->diag + lo, w->sc, w->red, 0);
     count_launch();
   }
-  D.allreduce(3);
+  st |= D.allreduce(3);
   D.stage(ST_XR);
+  return st || cudaPeekAtLastError() != cudaSuccess ? B200FEM_E_CUDA : 0;
 }
 
-// Same control flow as the single-GPU bicgstab (krylov.cu) with the collectives inserted.
-static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0, double rel_tol, double abs_tol,
-                         int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+// Jacobi-PCG iteration over the parts (krylov.cu enqueue_cg_iteration with the collectives):
+// halo of p + SpMV q = A p with p.Ap -> allreduce -> alpha; x, r, z = D^-1 r with r.r, r.z ->
+// allreduce -> beta; p = z + beta p.  Two allreduces and one halo per iteration.
+static int enqueue_dist_cg_iteration(Dist &D, double *const *x) {
+  const size_t np = D.parts.size();
+  std::vector<double *> pv(np);
+  std::vector<SpmvArgs> a(np);
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    a[p] = SpmvArgs{w->p, w->v, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
+    pv[p] = w->p;
+  }
+  int st = D.spmv(SP_PQ, a, pv.data(), 1);
+  st |= D.allreduce(1);
+  D.stage(ST_PQ);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_cg_update_xrz<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, x[p] + lo, w->r + lo, w->p + lo, w->v + lo,
+                                                             w->inv + lo, w->s + lo, w->sc, w->red, 0);
+    count_launch();
+  }
+  st |= D.allreduce(2);
+  D.stage(ST_CGXR);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_cg_update_p<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->s + lo, w->p + lo, w->sc);
+    count_launch();
+  }
+  return st || cudaPeekAtLastError() != cudaSuccess ? B200FEM_E_CUDA : 0;
+}
+
+// ---- batches of iterations as one CUDA graph (NCCL send/recv and allreduce captured with the
+// kernels; the overlap stream joins the capture through its fork/join events).  The graph is
+// captured at the first inner loop of a solve and relaunched per batch and per restart; the
+// host polls a device status snapshot double-buffered, as the eager loop does.  When the parts
+// do not share one stream, or capture fails (an NCCL build without graph support), the solve
+// falls back to enqueuing the iterations eagerly.  B200FEM_NO_GRAPH=1 forces the eager loop.
+constexpr int kDistGraphBatch = 8;
+
+struct BatchGraph {
+  cudaGraphExec_t exec = nullptr;
+  bool tried = false;
+  int64_t launches = 0;  // library kernels per graph launch
+  ~BatchGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+static bool dist_use_graph() {
+  static int v = -1;
+  if (v < 0) v = getenv("B200FEM_NO_GRAPH") ? 0 : 1;
+  return v == 1;
+}
+
+template <class F>
+static void capture_batch(Dist &D, BatchGraph &g, F &&enqueue_one) {
+  g.tried = true;
+  cudaStream_t s0 = D.stream(0);
+  for (size_t p = 1; p < D.parts.size(); ++p)
+    if (D.stream(p) != s0) return;
+  const int64_t l0 = g_launches.load();
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  int st = 0;
+  for (int i = 0; i < kDistGraphBatch; ++i) st |= enqueue_one();
+  cudaError_t e = cudaStreamEndCapture(s0, &graph);
+  g.launches = g_launches.load() - l0;
+  count_launch(-(int)g.launches);  // captured, not launched
+  if (st == 0 && e == cudaSuccess && graph) e = cudaGraphInstantiate(&g.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (st || e != cudaSuccess) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    cudaGetLastError();
+  }
+}
+
+// Runs iterations until the device status leaves KS_RUNNING; `poll` is the pinned snapshot
+// array (3 KrylovScalars) of part 0.  On return poll[0] holds the latest snapshot.
+template <class F>
+static int run_batches(Dist &D, BatchGraph &g, F &&enqueue_one, KrylovScalars *poll, b200fem_error *err) {
+  KrylovWork *w0 = D.parts[0]->m->kw;
+  cudaStream_t s0 = D.stream(0);
+  if (dist_use_graph() && !g.tried) capture_batch(D, g, enqueue_one);
+  int batch = 4, cur = 0;
+  auto enqueue_batch = [&](int slot) -> int {
+    if (g.exec) {
+      if (cudaGraphLaunch(g.exec, s0) != cudaSuccess) return B200FEM_E_CUDA;
+      count_launch((int)g.launches);
+    } else {
+      for (int i = 0; i < batch; ++i)
+        if (int st = enqueue_one()) return st;
+    }
+    B200_CUDA(cudaMemcpyAsync(poll + 1 + slot, w0->sc, sizeof(KrylovScalars), cudaMemcpyDeviceToHost, s0));
+    B200_CUDA(cudaEventRecord(w0->ev[slot], s0));
+    return 0;
+  };
+  if (int st = enqueue_batch(cur)) return set_err(err, st, "Krylov iteration enqueue failed"), st;
+  for (;;) {
+    batch = std::min(batch * 2, 16);
+    if (int st = enqueue_batch(cur ^ 1)) return set_err(err, st, "Krylov iteration enqueue failed"), st;
+    B200_CUDA_E(cudaEventSynchronize(w0->ev[cur]), err);
+    if (poll[1 + cur].status != KS_RUNNING) break;
+    cur ^= 1;
+  }
+  for (size_t p = 0; p < D.parts.size(); ++p) B200_CUDA_E(cudaStreamSynchronize(D.stream(p)), err);
+  *poll = poll[1 + (cur ^ 1)];  // latest snapshot (status is sticky)
+  B200_CUDA_E(cudaGetLastError(), err);
+  return 0;
+}
+
+// shared set-up of both distributed Krylov methods: workspaces, the local-comm result table,
+// the zero-diagonal check and ||b|| / the global DOF count (collectives)
+static int dist_setup(Dist &D, double *const *b, double rel_tol, double abs_tol, int64_t max_iters, double *tol,
+                      int64_t *max_it, b200fem_error *err) {
   const size_t np = D.parts.size();
   int64_t n_global_owned = 0;
   for (size_t p = 0; p < np; ++p) {
@@ -274,14 +396,13 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
     if (ensure_work(P->m)) return set_err(err, B200FEM_E_CUDA, "Krylov workspace allocation failed"), B200FEM_E_CUDA;
     n_global_owned += (P->own_hi - P->own_lo) * P->vec;
   }
-  if (D.comm->kind == 0 && np > 1) {
+  if (D.comm->kind == 0 && np > 1 && !D.res_dev) {
     std::vector<double *> rp(np);
     for (size_t p = 0; p < np; ++p) rp[p] = D.parts[p]->m->kw->red.result;
     B200_CUDA_E(dalloc(&D.res_dev, np), err);
     B200_CUDA_E(cudaMemcpy(D.res_dev, rp.data(), np * sizeof(double *), cudaMemcpyHostToDevice), err);
   }
-  // zero-diagonal check on owned rows, summed over ranks
-  for (size_t p = 0; p < np; ++p) {
+  for (size_t p = 0; p < np; ++p) {  // zero-diagonal check on owned rows, summed over ranks
     KrylovWork *w = D.parts[p]->m->kw;
     if (launch_diagonal(D.parts[p]->m, w->diag, w->inv, &w->red, nullptr)) return B200FEM_E_CUDA;
   }
@@ -293,14 +414,8 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
     set_err(err, B200FEM_E_ZERO_DIAGONAL, "zero diagonal entry; Jacobi preconditioner undefined");
     return B200FEM_E_ZERO_DIAGONAL;
   }
-  for (size_t p = 0; p < np; ++p) {
-    KrylovWork *w = D.parts[p]->m->kw;
-    if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x[p], 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
-    // ghost rows of the Krylov vectors are never computed: keep them finite
-    B200_CUDA_E(cudaMemsetAsync(w->v, 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
-  }
   if (D.dot(b, b, &bb)) return B200FEM_E_CUDA;
-  const double tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
+  *tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
   if (D.comm->kind == 1) {  // global DOF count for the default max_iters = 10 N
     double cnt = (double)n_global_owned;
     double *slot = D.parts[0]->m->kw->red.result;
@@ -310,13 +425,30 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
     B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
     n_global_owned = (int64_t)cnt;
   }
-  const int64_t max_it = max_iters > 0 ? max_iters : 10 * n_global_owned;
+  *max_it = max_iters > 0 ? max_iters : 10 * n_global_owned;
+  return 0;
+}
+
+// Same control flow as the single-GPU bicgstab (krylov.cu) with the collectives inserted.
+static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0, double rel_tol, double abs_tol,
+                         int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+  const size_t np = D.parts.size();
+  double tol = 0.0;
+  int64_t max_it = 0;
+  if (int st = dist_setup(D, b, rel_tol, abs_tol, max_iters, &tol, &max_it, err)) return st;
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x[p], 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+    // ghost rows of the Krylov vectors are never computed: keep them finite
+    B200_CUDA_E(cudaMemsetAsync(w->v, 0, D.parts[p]->m->n * sizeof(double), D.stream(p)), err);
+  }
   KrylovScalars H{};
   H.tol = tol;
   H.max_iters = max_it;
   long long it = 0, mv = 0, restarts = 0;
   double last_bd = -1.0;
   KrylovScalars *poll = D.parts[0]->m->kw->sc_host;
+  BatchGraph graph;  // captured at the first inner loop, relaunched at every restart
   for (;;) {
     H.status = KS_RUNNING;
     H.first = 1;
@@ -356,28 +488,7 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
       k_begin<<<1, 1, 0, D.stream(p)>>>(w->sc);
       count_launch();
     }
-    // batches of iterations with double-buffered status polling: the next batch is enqueued
-    // before the previous one is waited on, so the GPUs never idle on the host's launches
-    // (the collectives of a batch enqueued past convergence still run: batches stay <= 16)
-    KrylovWork *w0 = D.parts[0]->m->kw;
-    int batch = 4, cur = 0;
-    auto enqueue_batch = [&](int slot) -> int {
-      for (int i = 0; i < batch; ++i) enqueue_dist_iteration(D, x);
-      B200_CUDA(cudaMemcpyAsync(poll + 1 + slot, w0->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)));
-      B200_CUDA(cudaEventRecord(w0->ev[slot], D.stream(0)));
-      return 0;
-    };
-    if (enqueue_batch(cur)) return B200FEM_E_CUDA;
-    for (;;) {
-      batch = std::min(batch * 2, 16);
-      if (enqueue_batch(cur ^ 1)) return B200FEM_E_CUDA;
-      B200_CUDA_E(cudaEventSynchronize(w0->ev[cur]), err);
-      if (poll[1 + cur].status != KS_RUNNING) break;
-      cur ^= 1;
-    }
-    for (size_t p = 0; p < np; ++p) B200_CUDA_E(cudaStreamSynchronize(D.stream(p)), err);
-    *poll = poll[1 + (cur ^ 1)];  // latest snapshot (status is sticky)
-    B200_CUDA_E(cudaGetLastError(), err);
+    if (int st = run_batches(D, graph, [&] { return enqueue_dist_iteration(D, x); }, poll, err)) return st;
     it = poll->it;
     mv = poll->mv;
     if (poll->status == KS_BREAKDOWN) {
@@ -389,6 +500,77 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
         return B200FEM_E_BREAKDOWN;
       }
       last_bd = poll->res;
+    }
+  }
+}
+
+// Jacobi-PCG over the parts: the single-GPU pcg (krylov.cu) with the collectives inserted.
+static int dist_pcg(Dist &D, double *const *b, double *const *x, int has_x0, double rel_tol, double abs_tol,
+                    int64_t max_iters, b200fem_solve_info *info, b200fem_error *err) {
+  const size_t np = D.parts.size();
+  double tol = 0.0;
+  int64_t max_it = 0;
+  if (int st = dist_setup(D, b, rel_tol, abs_tol, max_iters, &tol, &max_it, err)) return st;
+  for (size_t p = 0; p < np; ++p) {
+    Matrix *m = D.parts[p]->m;
+    KrylovWork *w = m->kw;
+    if (!has_x0) B200_CUDA_E(cudaMemsetAsync(x[p], 0, m->n * sizeof(double), D.stream(p)), err);
+    B200_CUDA_E(cudaMemsetAsync(w->v, 0, m->n * sizeof(double), D.stream(p)), err);
+    B200_CUDA_E(cudaMemsetAsync(w->p, 0, m->n * sizeof(double), D.stream(p)), err);
+    if (m->n_dir) {  // x_d = b_d: the Krylov space then lives on the free rows (krylov.cu pcg)
+      k_set_dirichlet<<<grid_n(m->n_dir), kThreads, 0, D.stream(p)>>>(x[p], b[p], m->dir_dofs, m->n_dir);
+      count_launch();
+    }
+  }
+  KrylovScalars H{};
+  H.tol = tol;
+  H.max_iters = max_it;
+  long long it = 0, mv = 0, restarts = 0;
+  KrylovScalars *poll = D.parts[0]->m->kw->sc_host;
+  BatchGraph graph;
+  for (;;) {
+    H.status = KS_RUNNING;
+    H.it = it;
+    H.mv = mv;
+    for (size_t p = 0; p < np; ++p)
+      B200_CUDA_E(cudaMemcpyAsync(D.parts[p]->m->kw->sc, &H, sizeof(H), cudaMemcpyHostToDevice, D.stream(p)), err);
+    std::vector<SpmvArgs> ar(np);
+    for (size_t p = 0; p < np; ++p) {
+      KrylovWork *w = D.parts[p]->m->kw;
+      ar[p] = SpmvArgs{x[p], w->r, w->inv, w->diag, b[p], w->p, w->sc, 0};  // r = b - A x, p = D^-1 r
+    }
+    if (D.spmv(SP_CGRES, ar, x, 2)) return B200FEM_E_CUDA;
+    if (D.allreduce(2)) return B200FEM_E_CUDA;
+    D.stage(ST_CGRES);
+    ++restarts;
+    B200_CUDA_E(cudaMemcpyAsync(poll, D.parts[0]->m->kw->sc, sizeof(H), cudaMemcpyDeviceToHost, D.stream(0)), err);
+    B200_CUDA_E(cudaStreamSynchronize(D.stream(0)), err);
+    mv = poll->mv;
+    const double res = poll->res;
+    if (res <= tol) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      return 0;
+    }
+    if (it >= max_it) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
+      if (err) err->iterations = it, err->value = res;
+      set_err(err, B200FEM_E_LINEAR_SOLVER, "PCG did not converge in %lld iterations (residual %.3e, tol %.3e)",
+              (long long)max_it, res, tol);
+      return B200FEM_E_LINEAR_SOLVER;
+    }
+    for (size_t p = 0; p < np; ++p) {
+      k_begin_cg<<<1, 1, 0, D.stream(p)>>>(D.parts[p]->m->kw->sc);
+      count_launch();
+    }
+    if (int st = run_batches(D, graph, [&] { return enqueue_dist_cg_iteration(D, x); }, poll, err)) return st;
+    it = poll->it;
+    mv = poll->mv;
+    if (poll->status == KS_BREAKDOWN) {
+      if (info) *info = b200fem_solve_info{it, mv, restarts, poll->res, tol};
+      if (err) err->iterations = it, err->value = poll->res;
+      set_err(err, B200FEM_E_BREAKDOWN, "PCG breakdown at iteration %lld: p.Ap = %.3e <= 0 (operator not SPD)", it,
+              poll->r0v);
+      return B200FEM_E_BREAKDOWN;
     }
   }
 }
@@ -548,6 +730,22 @@ int b200fem_dist_bicgstab(b200fem_part **parts, int32_t np, b200fem_comm *comm, 
   }
   Dist D = make_dist(parts, np, comm);
   const int st = dist_bicgstab(D, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
+  cudaFree(D.res_dev);
+  return st;
+}
+
+int b200fem_dist_pcg(b200fem_part **parts, int32_t np, b200fem_comm *comm, double *const *b, double *const *x,
+                     int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters, b200fem_solve_info *info,
+                     b200fem_error *err) {
+  if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
+  if (info) memset(info, 0, sizeof(*info));
+  if (np < 1 || !comm || (((Comm *)comm)->kind == 1 && np != 1)) return B200FEM_E_INVALID;
+  if (!(rel_tol > 0) || !(abs_tol > 0)) {
+    set_err(err, B200FEM_E_INVALID, "linear solver tolerances must be positive");
+    return B200FEM_E_INVALID;
+  }
+  Dist D = make_dist(parts, np, comm);
+  const int st = dist_pcg(D, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
   cudaFree(D.res_dev);
   return st;
 }

@@ -291,6 +291,7 @@ class PartitionedSolver:
         self.comm = Communicator("nccl" if mode == "nccl" else "local", rank, world)
         ranks = [rank] if mode == "nccl" else list(range(nparts))
         self.plans = plan_parts(mesh, self.ranges, ranks)
+        self.operator = operator
         self.parts = [_Part(problem, p, operator) for p in self.plans]
         self._ptrs = (C.c_void_p * len(self.parts))(*[p.handle.value for p in self.parts])
 
@@ -324,14 +325,34 @@ class PartitionedSolver:
             p.ws.residual(p.problem, p.U, p.R, apply_dirichlet)
         return float(np.sqrt(self.dot("R", "R")))
 
-    def bicgstab(self, cfg: LinearSolveConfig) -> SolveStats:
+    def _check_operator(self, cfg: LinearSolveConfig):
+        """The parts' operators are built once (constructor ``operator``); a config asking for a
+        storage the parts do not have is an error, not a silent substitution."""
+        built = "grid" if all(p.grid for p in self.parts) else "csr"
+        want = cfg.operator
+        if want == "auto" or want == built or (want == "grid" and built == "grid"):
+            return
+        raise ValueError(f'LinearSolveConfig(operator="{want}") is not available on this PartitionedSolver: '
+                         f'its parts were built with the "{built}" operator (PartitionedSolver(..., operator=...))')
+
+    def linear_solve(self, cfg: LinearSolveConfig) -> SolveStats:
+        """rhs -> dU over all parts with cfg.method: "bicgstab" (reference) or "pcg"."""
+        self._check_operator(cfg)
+        if cfg.method not in ("bicgstab", "pcg"):
+            raise ValueError(f"unknown linear method {cfg.method!r}")
+        fn = _lib.lib().b200fem_dist_pcg if cfg.method == "pcg" else _lib.lib().b200fem_dist_bicgstab
         info = _lib.SolveInfo()
         err = _lib.Error()
-        st = _lib.lib().b200fem_dist_bicgstab(self._ptrs, len(self.parts), self.comm.handle, self._vec_ptrs("rhs"),
-                                              self._vec_ptrs("dU"), 0, float(cfg.rel_tol), float(cfg.abs_tol),
-                                              int(cfg.max_iters), C.byref(info), C.byref(err))
-        raise_for(st, err, "dist_bicgstab")
+        st = fn(self._ptrs, len(self.parts), self.comm.handle, self._vec_ptrs("rhs"), self._vec_ptrs("dU"), 0,
+                float(cfg.rel_tol), float(cfg.abs_tol), int(cfg.max_iters), C.byref(info), C.byref(err))
+        raise_for(st, err, f"dist_{cfg.method}")
         return SolveStats(info.iterations, info.matvecs, info.restarts, info.residual, info.tol)
+
+    def bicgstab(self, cfg: LinearSolveConfig) -> SolveStats:
+        """BiCGSTAB regardless of cfg.method (kept for callers of the round-1 API)."""
+        from dataclasses import replace
+
+        return self.linear_solve(replace(cfg, method="bicgstab"))
 
     def _dof_perm(self):
         vec = self.problem.vec
@@ -386,7 +407,7 @@ class PartitionedSolver:
                     p.assemble_tangent()
                     p._k_done = True
                 lib.b200fem_scale(p.problem.n_dofs, -1.0, D.ptr(p.R), D.ptr(p.rhs), stream)
-            lin.append(self.bicgstab(lin_cfg))
+            lin.append(self.linear_solve(lin_cfg))
             for p in self.parts:
                 lo, hi = p.own_dofs
                 lib.b200fem_axpy(hi - lo, 1.0, D.ptr(p.dU[lo:]), D.ptr(p.U[lo:]), stream)

@@ -161,8 +161,9 @@ def _tangent_matrix(problem, U, operator="csr"):
         if not (ws.has_grid and problem.vec == 3):
             raise ValueError('operator "grid32" needs a vec-3 box-lattice problem')
         K = ws._cache.get("newton_grid32")
-        if K is None:
-            K = GridOperator(ws)
+        if K is None:  # one FP64 GRID3 value buffer for both Newton operators (2.6 GB at config 3)
+            base = ws._cache.get("newton_grid")
+            K = GridOperator(ws, data=base.device_data if base is not None else None)
             ws._cache["newton_grid32"] = K
         ws.jacobian_grid(problem, U, K.device_data)
         K.refresh_f32()
@@ -174,7 +175,8 @@ def _tangent_matrix(problem, U, operator="csr"):
                 return K
         K = ws._cache.get("newton_grid")
         if K is None:
-            K = GridOperator(ws)
+            other = ws._cache.get("newton_grid32")
+            K = GridOperator(ws, data=other.device_data if other is not None else None)
             ws._cache["newton_grid"] = K
         ws.jacobian_grid(problem, U, K.device_data)
         if problem.jacobian_constant:
@@ -284,13 +286,19 @@ def tangent_transpose(problem, U) -> CsrMatrix:
 
 def newton_solve(problem, U0=None, cfg: NewtonConfig = NewtonConfig(),
                  lin_cfg: LinearSolveConfig = LinearSolveConfig()):
-    """Newton iteration on the assembled residual (solvers.py:198-227); returns (U, NewtonReport)."""
+    """Newton iteration on the assembled residual (solvers.py:198-227); returns (U, NewtonReport).
+
+    Runs on the workspace's stream (the one every assembly and Krylov kernel of this problem
+    is bound to), ordered after the caller's current stream and before its later work."""
     as_host = U0 is None or not D.is_device_tensor(U0)
-    workspace(problem)
-    U = D.zeros(problem.n_dofs) if U0 is None else D.to_device(U0, copy=True)
-    if tuple(U.shape) != (problem.n_dofs,):
-        raise ValueError(f"U0 must have shape ({problem.n_dofs},)")
-    U, rep = _newton_device(problem, U, cfg, lin_cfg)
+    ws = workspace(problem)
+    with ws.on_stream() as caller:
+        U = D.zeros(problem.n_dofs) if U0 is None else D.to_device(U0, copy=True)
+        if tuple(U.shape) != (problem.n_dofs,):
+            raise ValueError(f"U0 must have shape ({problem.n_dofs},)")
+        U, rep = _newton_device(problem, U, cfg, lin_cfg)
+        if caller is not None and not as_host:
+            U.record_stream(caller)
     return (D.to_host(U) if as_host else U), rep
 
 

@@ -188,10 +188,12 @@ class _NodeBlockOperator:
     _ctor = None
     _size = None
 
-    def __init__(self, ws):
+    def __init__(self, ws, data=None):
+        """``data``: share an existing value buffer (e.g. the FP64 GRID3 values of the "grid"
+        and "grid32" Newton operators; each re-assembles into it before use)."""
         self._ws = ws
         self._n = ws.n_dofs
-        self.device_data = D.empty(getattr(ws, self._size)())
+        self.device_data = D.empty(getattr(ws, self._size)()) if data is None else data
         self._handle = None
 
     @property

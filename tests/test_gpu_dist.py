@@ -92,3 +92,65 @@ def test_partitioned_grid3_parts(operator, nparts):
     rep = s.newton_solve(**TIGHT)
     assert rep.n_iterations == r1.n_iterations
     assert rel(s.gather_U(), U1) < 1e-9
+
+
+@pytest.mark.parametrize("operator", ["auto", "csr"])
+def test_partitioned_pcg_matches_single_gpu(operator):
+    """LinearSolveConfig(method="pcg") on the partitioned path runs the distributed Jacobi-PCG
+    (one halo + two allreduces per iteration) instead of silently running BiCGSTAB."""
+    case = dict(CASES["nh_block"], dims=(6, 5, 10))
+    lin = fem.LinearSolveConfig(method="pcg", rel_tol=1e-11, abs_tol=1e-13)
+    _, p1, _ = build("nh_block", case)
+    U1, r1 = fem.newton_solve(p1, cfg=TIGHT["cfg"], lin_cfg=lin)
+    _, p2, _ = build("nh_block", case)
+    s = PartitionedSolver(p2, nparts=3, mode="local", operator=operator)
+    rep = s.newton_solve(cfg=TIGHT["cfg"], lin_cfg=lin)
+    assert rep.n_iterations == r1.n_iterations
+    assert rel(s.gather_U(), U1) < 1e-9
+    # same Krylov method and counts as one GPU (the PCG recurrence is the same algorithm)
+    its1 = [st.iterations for st in r1.linear_stats]
+    its2 = [st.iterations for st in rep.linear_stats]
+    assert all(abs(a - b) <= max(2, 0.02 * a) for a, b in zip(its1, its2)), (its1, its2)
+
+
+def test_partitioned_rejects_operator_it_was_not_built_with():
+    _, p2, _ = build("nh_block", dict(CASES["nh_block"], dims=(4, 3, 8)))
+    s = PartitionedSolver(p2, nparts=2, mode="local", operator="csr")
+    with pytest.raises(ValueError, match="not available on this PartitionedSolver"):
+        s.newton_solve(lin_cfg=fem.LinearSolveConfig(operator="grid32"))
+
+
+def test_partitioned_graph_batches_equal_eager_loop():
+    """The captured batch graph replays exactly the eager enqueue: identical iterates."""
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, numpy as np
+sys.path[:0] = [os.environ["ROOT"], os.path.join(os.environ["ROOT"], "tests"), os.path.join(os.environ["ROOT"], "tests", "golden")]
+import paper_2212_00964_b200 as fem
+from cases import CASES
+from pkg_cases import build
+from paper_2212_00964_b200.distributed import PartitionedSolver
+_, p, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 10)))
+s = PartitionedSolver(p, nparts=3, mode="local")
+rep = s.newton_solve()
+np.save(sys.argv[1], s.gather_U())
+print([st.iterations for st in rep.linear_stats])
+'''
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for env_graph in ("1", None):
+            env = dict(os.environ, ROOT=root)
+            env.pop("B200FEM_NO_GRAPH", None)
+            if env_graph is None:
+                env["B200FEM_NO_GRAPH"] = "1"
+            f = os.path.join(d, f"u{len(outs)}.npy")
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append((np.load(f), r.stdout.strip()))
+    assert outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][0], outs[1][0])
