@@ -706,6 +706,296 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
   }
 }
 
+// ------------------------------------------------- jacobian phase A, node-lane mapping
+// Four cells per warp; lane (c, a) = (lane >> 3, lane & 7).
+//  1. lane (c, q) -- the same lanes read as (cell, Gauss point) -- computes the geometry, grad u,
+//     the law's scalars and the per-node vectors V_a(q) of its point for all 8 nodes a
+//     (NH: g, h = H g, u = F g; J2: g, y = s g; LE / Poisson: g) into shared memory;
+//  2. lane (c, a) then owns the symmetric pairs (a, (a + d) mod 8), d = 0..3 (and d = 4 for
+//     a < 4): 36 pairs over 8 lanes, 4 or 5 blocks in registers, accumulated over the 8 points.
+//     Per point a lane reads only the partner vectors V_b (9 doubles for NH) -- the operands it
+//     reuses (V_a, the coefficients) stay in registers -- so shared-memory wavefronts per cell
+//     drop ~3x against the pair-per-lane kernel above (its 858 wavefronts/cell made it
+//     L1-bound, profiles/r01_ncu_jacobian_nh.json).
+// Block algebra (same as above, with w_b = c3 h_b - c2 u_b formed on the fly):
+//   NH:  K_ik += c1 d_ik (g_a.g_b) + h_a,i w_b,k - c2 u_a,i h_b,k + c4 h_a,k h_b,i
+//   J2:  K_ik += c1 d_ik (g_a.g_b) + cl g_a,i g_b,k + c1 g_a,k g_b,i + c3 y_a,i y_b,k
+//   LE:  J2 without the y term;  Poisson: c1 (g_a.g_b)
+// Shared-memory strides are padded so that every access pattern is bank-conflict free.
+constexpr int kJac2Warps = 4;
+
+template <int MAT>
+struct Jac2Cfg {
+  static constexpr int VEC = (MAT == B200FEM_MAT_POISSON) ? 1 : 3;
+  static constexpr int NV = (MAT == B200FEM_MAT_NH) ? 9 : (MAT == B200FEM_MAT_J2) ? 6 : 3;  // vector doubles
+  static constexpr int QS = 8 * NV + 1;   // point stride (odd: conflict-free across points)
+  static constexpr int CS = 8 * QS;       // cell stride = 64 NV + 8 = 8 (mod 16): two cells 16 banks apart
+  static_assert(CS % 16 == 8, "cell stride must be 8 mod 16 doubles");
+  // dynamic shared memory (doubles): dN table [q][25] | X,U [w][c][k][7] | V [w][4 CS] | coef [w][160]
+  static constexpr int SM_DN = 8 * 25, SM_XU = kJac2Warps * 4 * 8 * 7, SM_V = kJac2Warps * 4 * CS,
+                       SM_C = kJac2Warps * 160;
+  static constexpr size_t BYTES = sizeof(double) * (SM_DN + SM_XU + SM_V + SM_C);
+};
+
+// Phase A of four cells (one per 8-lane group c = lane >> 3; cell e of this lane's group,
+// `valid` false for padding lanes): on return lane (c, a) holds in K[d] the block of the pair
+// (a, (a + d) mod 8), d = 0..3 (and 4 for a < 4), as K_{(a,i),(b,k)}.  Element errors are
+// flagged on the device (DevErr) exactly as the other element kernels do.
+template <int MAT>
+__device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, bool valid, int lane,
+                                                 const double *__restrict__ sdN, double (*sXUw)[8][7], double *V,
+                                                 double *Cf, double (&K)[5][Jac2Cfg<MAT>::VEC * Jac2Cfg<MAT>::VEC]) {
+  using CF = Jac2Cfg<MAT>;
+  constexpr int VEC = CF::VEC, NV = CF::NV, QS = CF::QS, CS = CF::CS;
+  constexpr int NB = 5, BB = VEC * VEC;
+  const int c = lane >> 3, a8 = lane & 7;
+  {  // node a8 of cell c: coordinates and U
+    const int node = a.cells[e * 8 + a8];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sXUw[c][a8][d] = a.coords[(int64_t)node * 3 + d];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) sXUw[c][a8][3 + v] = a.U[(int64_t)node * VEC + v];
+  }
+  __syncwarp();
+  {  // ---- 1. lane (c, q): point quantities and the per-node vectors
+    const int q = a8;
+    double Jm[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double Gr[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // sum_k U_k (x) dphi_k (reference gradient)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double d0 = sdN[q * 25 + k * 3], d1 = sdN[q * 25 + k * 3 + 1], d2 = sdN[q * 25 + k * 3 + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double x = sXUw[c][k][i];
+        Jm[i][0] = fma(x, d0, Jm[i][0]);
+        Jm[i][1] = fma(x, d1, Jm[i][1]);
+        Jm[i][2] = fma(x, d2, Jm[i][2]);
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const double u = sXUw[c][k][3 + v];
+        Gr[v][0] = fma(u, d0, Gr[v][0]);
+        Gr[v][1] = fma(u, d1, Gr[v][1]);
+        Gr[v][2] = fma(u, d2, Gr[v][2]);
+      }
+    }
+    const double A0 = Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1], B0 = Jm[0][2] * Jm[2][1] - Jm[0][1] * Jm[2][2];
+    const double C0 = Jm[0][1] * Jm[1][2] - Jm[0][2] * Jm[1][1], D0 = Jm[1][2] * Jm[2][0] - Jm[1][0] * Jm[2][2];
+    const double E0 = Jm[0][0] * Jm[2][2] - Jm[0][2] * Jm[2][0], F0 = Jm[0][2] * Jm[1][0] - Jm[0][0] * Jm[1][2];
+    const double G0 = Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0], H0 = Jm[0][1] * Jm[2][0] - Jm[0][0] * Jm[2][1];
+    const double I0 = Jm[0][0] * Jm[1][1] - Jm[0][1] * Jm[1][0];
+    const double jxw = Jm[0][0] * A0 + Jm[0][1] * D0 + Jm[0][2] * G0;
+    const double r = 1.0 / jxw;
+    // G_k[aa] = sum_m inv[m][aa] dphi_k[m]  (elements.py:130)
+    const double inv[3][3] = {{A0 * r, B0 * r, C0 * r}, {D0 * r, E0 * r, F0 * r}, {G0 * r, H0 * r, I0 * r}};
+    double scale = jxw;
+    if (a.mp.simp) scale *= pow(a.theta[e], a.mp.penalty);
+    double gu[3][3];
+    double gs = 0.0;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        gu[v][d] = Gr[v][0] * inv[0][d] + Gr[v][1] * inv[1][d] + Gr[v][2] * inv[2][d];
+        gs += fabs(gu[v][d]);
+      }
+    bool vfin = isfinite(gs), fin = true, bad_def = false;
+    double detF = 1.0;
+    double cf[4] = {0.0, 0.0, 0.0, 0.0};
+    double M1[3][3], M2[3][3];  // NH: F, H; J2: s (deviator)
+    if (MAT == B200FEM_MAT_POISSON) {
+      cf[0] = a.mp.alpha * scale;
+    } else if (MAT == B200FEM_MAT_LE) {
+      cf[0] = a.mp.mu * scale;
+      cf[1] = a.mp.lam * scale;
+    } else if (MAT == B200FEM_MAT_NH) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) M1[i][j] = gu[i][j] + (i == j ? 1.0 : 0.0);
+      const double J = det3(M1);
+      detF = J;
+      if (!(J <= 0.0)) {
+        inv_transpose(M1, J, M2);
+      } else {
+        bad_def = true;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) M2[i][j] = 0.0;
+      }
+      double I1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) I1 += M1[i][j] * M1[i][j];
+      vfin = vfin && isfinite(J) && isfinite(I1);
+      const double rc = bad_def ? 0.0 : rcbrt(J);
+      const double Ga = a.mp.mu * (rc * rc);  // G J^{-2/3}
+      cf[0] = Ga * scale;
+      cf[1] = (2.0 / 3.0) * Ga * scale;
+      cf[2] = ((2.0 / 9.0) * Ga * I1 + a.mp.kappa * J * (2.0 * J - 1.0)) * scale;
+      cf[3] = ((1.0 / 3.0) * Ga * I1 - a.mp.kappa * J * (J - 1.0)) * scale;
+      fin = isfinite(cf[0]) && isfinite(cf[1]) && isfinite(cf[2]) && isfinite(cf[3]);
+    } else {  // J2 consistent tangent (derivative of j2_return_map incl. the s = 0 guard)
+      const double *ep = a.eps_prev + (e * 8 + q) * 9;
+      const double *sp = a.sig_prev + (e * 8 + q) * 9;
+      double st[3][3], seff;
+      bool pos;
+      j2_trial(gu, ep, sp, a.mp, st, M1, seff, pos);
+      const double over = fmax(seff - a.mp.sy, 0.0);
+      const double f = over / seff;
+      const double active = (seff - a.mp.sy > 0.0) ? 1.0 : 0.0;  // ramp'(0) = 0
+      const double gam = pos ? (active / seff - over / (seff * seff)) * 3.0 * a.mp.mu / seff : 0.0;
+      const double beta = 2.0 * a.mp.mu * f;
+      cf[0] = (a.mp.mu - 0.5 * beta) * scale;
+      cf[1] = (a.mp.lam + beta / 3.0) * scale;
+      cf[2] = -gam * scale;
+      fin = isfinite(cf[0]) && isfinite(cf[1]) && isfinite(cf[2]);
+      vfin = vfin && isfinite(seff) && isfinite(st[0][0] + st[1][1] + st[2][2]);
+    }
+    if (valid) {
+      const unsigned long long key = (unsigned long long)e * 8 + q;
+      if (bad_def) {
+        atomicMin(&a.derr->inv_def, key);
+        atomicMin(&a.derr->min_detF, ord_bits(detF));
+      } else if (!vfin) {
+        atomicMin(&a.derr->nonfin_v, key);
+      } else if (!fin) {
+        atomicMin(&a.derr->nonfin_d, key);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Cf[c * 40 + q * 5 + j] = cf[j];
+    double *Vq = V + c * CS + q * QS;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double d0 = sdN[q * 25 + k * 3], d1 = sdN[q * 25 + k * 3 + 1], d2 = sdN[q * 25 + k * 3 + 2];
+      double g[3];
+#pragma unroll
+      for (int aa = 0; aa < 3; ++aa) g[aa] = inv[0][aa] * d0 + inv[1][aa] * d1 + inv[2][aa] * d2;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) Vq[k * NV + d] = g[d];
+      if (MAT == B200FEM_MAT_NH) {  // h = H g (slot 3), u = F g (slot 6)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          Vq[k * NV + 3 + i] = M2[i][0] * g[0] + M2[i][1] * g[1] + M2[i][2] * g[2];
+          Vq[k * NV + 6 + i] = M1[i][0] * g[0] + M1[i][1] * g[1] + M1[i][2] * g[2];
+        }
+      } else if (MAT == B200FEM_MAT_J2) {  // y = s g (slot 3)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) Vq[k * NV + 3 + i] = M1[i][0] * g[0] + M1[i][1] * g[1] + M1[i][2] * g[2];
+      }
+    }
+  }
+  __syncwarp();
+  // ---- 2. lane (c, a): pairs (a, a + d mod 8)
+#pragma unroll
+  for (int d = 0; d < NB; ++d)
+#pragma unroll
+    for (int t = 0; t < BB; ++t) K[d][t] = 0.0;
+  const int ia = a8;
+#pragma unroll 1
+  for (int q = 0; q < 8; ++q) {
+    const double *Vq = V + c * CS + q * QS;
+    const double c1 = Cf[c * 40 + q * 5], c2 = Cf[c * 40 + q * 5 + 1], c3 = Cf[c * 40 + q * 5 + 2],
+                 c4 = Cf[c * 40 + q * 5 + 3];
+    double va[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) va[j] = Vq[ia * NV + j];
+    // a-side operands (registers): NH: h_a, -c2 u_a, c4 h_a;  J2: cl g_a, c1 g_a, c3 y_a
+    double A1[3], A2[3], A3[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (MAT == B200FEM_MAT_NH) {
+        A1[i] = va[3 + i];
+        A2[i] = -c2 * va[6 + i];
+        A3[i] = c4 * va[3 + i];
+      } else {
+        A1[i] = c2 * va[i];  // cl g_a (c2 slot holds cl for LE / J2)
+        A2[i] = c1 * va[i];
+        A3[i] = (MAT == B200FEM_MAT_J2) ? c3 * va[3 + i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < NB; ++d) {
+      if (d == 4 && ia >= 4) break;
+      const int b = (ia + d) & 7;
+      double vb[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) vb[j] = (d == 0) ? va[j] : Vq[b * NV + j];
+      const double gg = va[0] * vb[0] + va[1] * vb[1] + va[2] * vb[2];
+      if (MAT == B200FEM_MAT_POISSON) {
+        K[d][0] = fma(c1, gg, K[d][0]);
+      } else {
+        const double dg = c1 * gg;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) K[d][i * 3 + i] += dg;
+        if (MAT == B200FEM_MAT_NH) {
+          double wb[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) wb[k] = c3 * vb[3 + k] - c2 * vb[6 + k];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              K[d][i * 3 + k] = fma(A1[i], wb[k], fma(A2[i], vb[3 + k], fma(A3[k], vb[3 + i], K[d][i * 3 + k])));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              double t = fma(A1[i], vb[k], fma(A2[k], vb[i], K[d][i * 3 + k]));
+              if (MAT == B200FEM_MAT_J2) t = fma(A3[i], vb[3 + k], t);
+              K[d][i * 3 + k] = t;
+            }
+        }
+      }
+    }
+  }
+}
+
+template <int MAT>
+__global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, int64_t n, double *__restrict__ Ke,
+                                                                    int soa) {
+  using CF = Jac2Cfg<MAT>;
+  constexpr int VEC = CF::VEC, CS = CF::CS;
+  constexpr int NB = 5, BB = VEC * VEC;
+  extern __shared__ double jac2_sm[];
+  double *sdN = jac2_sm;                                                     // [q][k*3 + d], point stride 25
+  double(*sXU)[4][8][7] = reinterpret_cast<double(*)[4][8][7]>(jac2_sm + CF::SM_DN);  // [w][c][k][X, U]
+  for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3;
+  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * 4 * CS;                  // [c][q][a][NV]
+  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;         // [c][q][4], point stride 5
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
+    const bool valid = base + c < n;
+    const int64_t e = valid ? base + c : n - 1;
+    double K[NB][BB];
+    jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
+    const int ia = lane & 7;
+    if (valid) {
+#pragma unroll
+      for (int d = 0; d < NB; ++d) {
+        if (d == 4 && ia >= 4) break;
+        const int b = (ia + d) & 7;
+        const int lo = ia < b ? ia : b, hi = ia < b ? b : ia;
+        const int p = lo * (15 - lo) / 2 + hi;  // upper-triangle index of (lo, hi)
+        double Kt[VEC][VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) Kt[i][k] = (ia <= b) ? K[d][i * VEC + k] : K[d][k * VEC + i];
+        jac_store<VEC>(Ke, e, n, p, soa, Kt);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Warp per node: the node's VEC rows (contiguous in the CSR values) are accumulated in
 // shared memory from its incident cells in ascending cell id -- every CSR slot sums its
 // contributions in the reference's order (assembly.py:296, kernels.py:30-34) -- then
@@ -1220,28 +1510,253 @@ __global__ void __launch_bounds__(kThreads) k_csr_pull(const double *__restrict_
   }
 }
 
+// ------------------------------------------ fused lattice tangent (GRID3, vec 3, box meshes)
+// One CTA per 8 x 8 column of cells, marching the cell layers k = 0 .. NZ-2.  Per layer the
+// 64 cells are processed in 4 parity colours ((i, j) mod 2: cells of one colour share no node),
+// 16 cells per colour = 4 warps x 4 cells of the phase-A device function above; each lane adds
+// its cell blocks straight into the column's node-block accumulators in shared memory (fixed
+// colour order -> deterministic, no atomics).  Node plane k is complete after layer k (its
+// in-plane blocks carry layer k-1's contributions, its +z blocks have only layer k's), so it is
+// written out as GRID3 blocks and the next plane's in-plane partial sums become the carry.
+// The 6.5 GB per-cell block scratch and the lattice pull of the two-phase path disappear; only
+// nodes on the column's side faces (shared with a neighbouring column) are written as per-column
+// partial blocks and summed by k_grid_edge_finish in a fixed column order.
+constexpr int kFT = 8;                         // cells per column side
+constexpr int kFN = kFT + 1;                   // nodes per column side
+constexpr int kFNodes = kFN * kFN;             // 81
+constexpr int kFAcc = 14 * 9 + 1;              // node stride of the plane accumulator (odd)
+constexpr int kFNext = 5 * 9;                  // in-plane blocks carried to the next plane
+
+template <int MAT>
+struct FusedCfg {
+  using CF = Jac2Cfg<MAT>;
+  static constexpr int SM_ACC = kFNodes * kFAcc, SM_NEXT = kFNodes * kFNext;
+  static constexpr size_t BYTES = CF::BYTES + sizeof(double) * (SM_ACC + SM_NEXT);
+};
+
+// which side-face "edge line" a lattice node (i, j) lies on, or -1 (interior / mesh boundary);
+// x-lines (i = kFT m, 0 < i < nxc) first, then y-lines (j = kFT l, 0 < j < nyc)
+__device__ __forceinline__ int64_t edge_line(int i, int j, int NX, int NY) {
+  const int nxc = NX - 1, nyc = NY - 1;
+  const int mx = (nxc + kFT - 1) / kFT;
+  if (i % kFT == 0 && i > 0 && i < nxc) return (int64_t)(i / kFT - 1) * NY + j;
+  if (j % kFT == 0 && j > 0 && j < nyc) return (int64_t)(mx - 1) * NY + (int64_t)(j / kFT - 1) * NX + i;
+  return -1;
+}
+
+template <int MAT>
+__global__ void __launch_bounds__(kJac2Warps * 32, 1) k_tangent_grid_fused(ElemArgs a, int NX, int NY, int NZ,
+                                                                           int64_t gnpad, double *__restrict__ grid,
+                                                                           double *__restrict__ part) {
+  using CF = Jac2Cfg<MAT>;
+  static_assert(CF::VEC == 3, "vec-3 laws only");
+  constexpr int CS = CF::CS;
+  extern __shared__ double jac2_sm[];
+  double *sdN = jac2_sm;
+  double(*sXU)[4][8][7] = reinterpret_cast<double(*)[4][8][7]>(jac2_sm + CF::SM_DN);
+  double *acc = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + CF::SM_C;  // [node][14 kinds][9], stride kFAcc
+  double *nxt = acc + FusedCfg<MAT>::SM_ACC;                             // [node][5 kinds][9]
+  for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
+  for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_ACC; t += blockDim.x) acc[t] = 0.0;
+  for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_NEXT; t += blockDim.x) nxt[t] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3, ia = lane & 7;
+  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * 4 * CS;
+  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;
+  const int nxc = NX - 1, nyc = NY - 1, nzc = NZ - 1;
+  const int mx = (nxc + kFT - 1) / kFT;
+  const int tx = blockIdx.x % mx, ty = blockIdx.x / mx;
+  const int i0 = tx * kFT, j0 = ty * kFT;
+  const int64_t nxy = (int64_t)NX * NY;
+  const int64_t n_lines = (int64_t)(mx - 1) * NY + (int64_t)(((nyc + kFT - 1) / kFT) - 1) * NX;
+
+  // write node plane `pk` of the column: interior nodes -> GRID3, side-face nodes -> partial slot
+  auto emit = [&](int pk, int kinds) {
+    for (int t = threadIdx.x; t < kFNodes * 126; t += blockDim.x) {
+      const int node = t % kFNodes, ke = t / kFNodes, kind = ke / 9;
+      const int li = node % kFN, lj = node / kFN, i = i0 + li, j = j0 + lj;
+      if (i >= NX || j >= NY || kind >= kinds) continue;
+      if (edge_line(i, j, NX, NY) >= 0) continue;
+      const int64_t n = i + (int64_t)NX * j + nxy * pk;
+      grid[grid_idx(kind, ke % 9, n, gnpad)] = acc[node * kFAcc + ke];
+    }
+    for (int node = w; node < kFNodes; node += kJac2Warps) {  // warp per side-face node
+      const int li = node % kFN, lj = node / kFN, i = i0 + li, j = j0 + lj;
+      if (i >= NX || j >= NY) continue;
+      const int64_t line = edge_line(i, j, NX, NY);
+      if (line < 0) continue;
+      const int slot = ((li == 0 && i % kFT == 0 && i > 0) ? 1 : 0) + ((lj == 0 && j % kFT == 0 && j > 0) ? 2 : 0);
+      double *o = part + (((int64_t)pk * n_lines + line) * 4 + slot) * 126;
+      for (int ke = lane; ke < 126; ke += 32) o[ke] = (ke / 9 < kinds) ? acc[node * kFAcc + ke] : 0.0;
+    }
+  };
+
+  for (int k = 0; k < nzc; ++k) {
+#pragma unroll 1
+    for (int color = 0; color < 4; ++color) {
+      const int ci = (color & 1) + 2 * c, cj = (color >> 1) + 2 * w;
+      const int gx = i0 + ci, gy = j0 + cj;
+      const bool valid = gx < nxc && gy < nyc;
+      const int64_t e = valid ? gx + (int64_t)nxc * (gy + (int64_t)nyc * k) : 0;
+      double K[5][9];
+      jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
+      if (valid) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          if (d == 4 && ia >= 4) break;
+          const int b = (ia + d) & 7;
+          // VTK vertex positions (mesh.py:159-167): a = lz*4 + {0:(0,0),1:(1,0),2:(1,1),3:(0,1)}
+          const int ax = ((ia & 3) == 1 || (ia & 3) == 2), ay = ((ia & 3) >= 2), az = ia >> 2;
+          const int bx = ((b & 3) == 1 || (b & 3) == 2), by = ((b & 3) >= 2), bz = b >> 2;
+          // owner = the lower node id (lexicographic z, y, x); the block of (owner, other)
+          const bool a_owns = (az != bz) ? az < bz : (ay != by) ? ay < by : ax <= bx;
+          const int ox = a_owns ? ax : bx, oy = a_owns ? ay : by, oz = a_owns ? az : bz;
+          const int kind = grid_index(a_owns ? bx - ax : ax - bx, a_owns ? by - ay : ay - by,
+                                      a_owns ? bz - az : az - bz);
+          const int node = (ci + ox) + kFN * (cj + oy);
+          double *dst = (oz == 0) ? acc + node * kFAcc + kind * 9 : nxt + node * kFNext + kind * 9;
+#pragma unroll
+          for (int ii = 0; ii < 3; ++ii)
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) dst[ii * 3 + kk] += a_owns ? K[d][ii * 3 + kk] : K[d][kk * 3 + ii];
+        }
+      }
+      __syncthreads();  // colour order: every node block sums its cells in a fixed order
+    }
+    emit(k, 14);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kFNodes * 126; t += blockDim.x) {  // plane k+1: carry in, rest zero
+      const int node = t / 126, ke = t % 126;
+      acc[node * kFAcc + ke] = ke < kFNext ? nxt[node * kFNext + ke] : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_NEXT; t += blockDim.x) nxt[t] = 0.0;
+    __syncthreads();
+  }
+  emit(nzc, 5);  // the top plane: in-plane blocks from the last layer only
+}
+
+// side-face nodes: GRID3 block = sum of the columns' partial blocks in slot order (fixed)
+__global__ void __launch_bounds__(kThreads) k_grid_edge_finish(int NX, int NY, int NZ, int64_t gnpad,
+                                                               const double *__restrict__ part,
+                                                               double *__restrict__ grid) {
+  const int nxc = NX - 1, nyc = NY - 1;
+  const int mx = (nxc + kFT - 1) / kFT, my = (nyc + kFT - 1) / kFT;
+  const int64_t n_lines = (int64_t)(mx - 1) * NY + (int64_t)(my - 1) * NX;
+  const int64_t total = n_lines * NZ * 126;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int ke = (int)(t % 126);
+    const int64_t lp = t / 126, line = lp % n_lines, pk = lp / n_lines;
+    int i, j;
+    if (line < (int64_t)(mx - 1) * NY) {
+      i = (int)(line / NY + 1) * kFT;
+      j = (int)(line % NY);
+    } else {
+      const int64_t r = line - (int64_t)(mx - 1) * NY;
+      j = (int)(r / NX + 1) * kFT;
+      i = (int)(r % NX);
+    }
+    if (edge_line(i, j, NX, NY) != line) continue;  // a y-line slot of an x-line node: unused
+    const bool xe = i % kFT == 0 && i > 0 && i < nxc, ye = j % kFT == 0 && j > 0 && j < nyc;
+    const double *p = part + ((pk * n_lines + line) * 4) * 126 + ke;
+    double v = p[0];
+    if (xe) v += p[126];
+    if (ye) v += p[2 * 126];
+    if (xe && ye) v += p[3 * 126];
+    grid[grid_idx(ke / 9, ke % 9, i + (int64_t)NX * j + (int64_t)NX * NY * pk, gnpad)] = v;
+  }
+}
+
+static int64_t fused_part_doubles(int NX, int NY, int NZ) {
+  const int mx = (NX - 1 + kFT - 1) / kFT, my = (NY - 1 + kFT - 1) / kFT;
+  return ((int64_t)(mx - 1) * NY + (int64_t)(my - 1) * NX) * NZ * 4 * 126;
+}
+
+template <int MAT>
+static void launch_fused(Ctx *c, cudaStream_t s, const ElemArgs &a, double *grid) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tangent_grid_fused<MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)FusedCfg<MAT>::BYTES);
+    attr = true;
+  }
+  const int mx = (c->grid_nx - 1 + kFT - 1) / kFT, my = (c->grid_ny - 1 + kFT - 1) / kFT;
+  k_tangent_grid_fused<MAT><<<mx * my, kJac2Warps * 32, FusedCfg<MAT>::BYTES, s>>>(
+      a, c->grid_nx, c->grid_ny, c->grid_nz, c->grid_npad, grid, c->scratch);
+  const int64_t total = fused_part_doubles(c->grid_nx, c->grid_ny, c->grid_nz) / 4;
+  if (total > 0)
+    k_grid_edge_finish<<<grid_cap(total, kThreads), kThreads, 0, s>>>(c->grid_nx, c->grid_ny, c->grid_nz,
+                                                                     c->grid_npad, c->scratch, grid);
+  count_launch(2);
+}
+
+template <int MAT>
+static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, double *Ke, int soa) {
+  static bool attr = false;  // > 48 KB of shared memory is opt-in per kernel
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobian_v2<MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Jac2Cfg<MAT>::BYTES);
+    attr = true;
+  }
+  k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
+}
+
+// B200FEM_TANGENT = v1 (pair-per-lane phase A) | v2 (node-lane phase A) | fused (lattice column
+// kernel for the GRID3 tangent; v2 elsewhere).  Read once per process.
+static int tangent_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("B200FEM_TANGENT");
+    v = !e ? 0 : !strcmp(e, "v2") ? 1 : !strcmp(e, "fused") ? 2 : 0;
+  }
+  return v;
+}
+
 // Two-phase Jacobian: (1) the 36 symmetric 3x3 blocks of every cell's Ke into scratch,
 // (2) warp-per-node ordered gather writing each CSR row segment exactly once.
 int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, double *sym, double *grid) {
   cudaStream_t s = c->stream;
   const int vv = c->vec * c->vec;
-  if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
-  const ElemArgs a = make_args(c, U);
   // GRID-only tangent on a lattice: element-major scratch + lattice pull instead of the gather
   // (element-major scratch for vec 1; vec 3 keeps the cell-major blocks, whose 72-byte rows the
   // pull reads whole -- element-major stores of a warp-per-cell kernel would be partial sectors)
   const bool pull = grid && !data && !sym && c->grid_nx && !getenv("B200FEM_NO_GRID_PULL");
+  if (pull && c->vec == 3 && tangent_variant() == 2 && c->grid_nx > 1 && c->grid_ny > 1 && c->grid_nz > 1) {
+    // fused column kernel: no per-cell scratch (the scratch holds the side-face partials)
+    if (ensure_scratch(c, (size_t)std::max<int64_t>(1, fused_part_doubles(c->grid_nx, c->grid_ny, c->grid_nz)),
+                       err))
+      return B200FEM_E_CUDA;
+    const ElemArgs a2 = make_args(c, U);
+    switch (c->material) {
+      case B200FEM_MAT_LE: launch_fused<B200FEM_MAT_LE>(c, s, a2, grid); break;
+      case B200FEM_MAT_NH: launch_fused<B200FEM_MAT_NH>(c, s, a2, grid); break;
+      default: launch_fused<B200FEM_MAT_J2>(c, s, a2, grid); break;
+    }
+    B200_CUDA_E(cudaGetLastError(), err);
+    return fetch_element_errors(c, err, true);
+  }
+  if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
+  const ElemArgs a = make_args(c, U);
   // reference CSR layout on a scalar lattice: the same pull (assemble_jacobian, operator="csr").
   // Not for vec 3: a thread's 27 blocks land in 3 rows ~2 KB apart from its neighbours' -- the
   // uncoalesced 8-byte stores made it 21 ms against 13.7 ms for the gather (config 3)
   const bool csr_pull = !grid && data && !sym && c->grid_nx && c->vec == 1 && !getenv("B200FEM_NO_GRID_PULL");
   const int soa = ((pull || csr_pull) && c->vec == 1) ? 1 : 0;
-  const int g = grid_cap(c->n_cells, kJacWarps);
-  switch (c->material) {
-    case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
-    case B200FEM_MAT_LE: k_jacobian<B200FEM_MAT_LE><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
-    case B200FEM_MAT_NH: k_jacobian<B200FEM_MAT_NH><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
-    default: k_jacobian<B200FEM_MAT_J2><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+  if (tangent_variant() == 0) {  // A/B: the pair-per-lane phase A
+    const int g = grid_cap(c->n_cells, kJacWarps);
+    switch (c->material) {
+      case B200FEM_MAT_POISSON: k_jacobian<B200FEM_MAT_POISSON><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+      case B200FEM_MAT_LE: k_jacobian<B200FEM_MAT_LE><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+      case B200FEM_MAT_NH: k_jacobian<B200FEM_MAT_NH><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+      default: k_jacobian<B200FEM_MAT_J2><<<g, kJacWarps * 32, 0, s>>>(a, c->n_cells, c->scratch, soa); break;
+    }
+  } else {
+    const int g = grid_cap(c->n_cells, kJac2Warps * 4);
+    switch (c->material) {
+      case B200FEM_MAT_POISSON: launch_jac2<B200FEM_MAT_POISSON>(g, s, a, c->n_cells, c->scratch, soa); break;
+      case B200FEM_MAT_LE: launch_jac2<B200FEM_MAT_LE>(g, s, a, c->n_cells, c->scratch, soa); break;
+      case B200FEM_MAT_NH: launch_jac2<B200FEM_MAT_NH>(g, s, a, c->n_cells, c->scratch, soa); break;
+      default: launch_jac2<B200FEM_MAT_J2>(g, s, a, c->n_cells, c->scratch, soa); break;
+    }
   }
   if (pull) {
     const int64_t nn = c->n_nodes;
