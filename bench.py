@@ -10,9 +10,10 @@ resident in HBM.  `e2e` is the same solve through the public API with host buffe
 (U0 from pinned host memory in, U to host out).  Inputs (CSR values 4.9 GB) are far
 larger than the 126 MB L2, so no explicit flush is needed between steps.
 
---impl reference times the reference algorithm on the host CPU (the numpy/numba oracle
-port of gradfem, all host threads) on a bounded sample and extrapolates to the same
-config; it prints the same metric.
+--impl reference times the reference package itself (gradfem, pip-installed into
+baseline/_ref) on the host CPU with all host threads: every phase rate is measured live
+(Jacobian / residual at a small mesh, matvec and BiCGSTAB on the full 136^3 sparsity) and
+composed to the config-3 solve; it prints the same metric.
 """
 
 import argparse
@@ -41,7 +42,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=136)
     p.add_argument("--stretch", type=float, default=0.02)
-    p.add_argument("--cpu-sample-n", type=int, default=20)
+    p.add_argument("--ref-cell-n", type=int, default=10,
+                   help="reference arm: mesh edge of the live Jacobian / residual sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--linear", default="bicgstab", choices=["bicgstab", "pcg"],
                    help="Krylov method of the timed Newton solve (reference default: bicgstab)")
@@ -76,74 +78,23 @@ def config(n, stretch):
 
 
 # ------------------------------------------------------------------ CPU reference sample
-def cpu_reference_sample(n_s, n_target, stretch):
-    """Reference algorithm on the host (oracle port of gradfem: numpy element kernels,
-    numba prange CSR matvec = kernels.py:21-28, BiCGSTAB = solvers.py:87-167) on an n_s^3
-    sample of the same problem; phase rates extrapolated to n_target^3."""
-    import oracle as orc
-    try:
-        import numba
-    except Exception:
-        numba = None
-    nodes, cells = orc.box_mesh(n_s, n_s, n_s, 1.0, 1.0, 1.0)
-    law = orc.Law("nh", E=70e3, nu=0.3, sigma_yield=250.0)
-    bot = np.flatnonzero(np.abs(nodes[:, 2]) <= 1e-5)
-    top = np.flatnonzero(np.abs(nodes[:, 2] - 1.0) <= 1e-5)
-    dd = np.concatenate([bot * 3 + c for c in range(3)] + [top * 3 + 2])
-    dv = np.concatenate([np.zeros(3 * bot.size), np.full(top.size, stretch)])
-    o = np.argsort(dd)
-    prob = orc.OracleProblem(nodes, cells, law, dd[o], dv[o])
-    U0 = np.zeros(prob.n_dofs)
-    x = np.random.default_rng(0).standard_normal(prob.n_dofs)
-    K = orc.jacobian(prob, U0)
-    orc.csr_matvec(prob.indptr, prob.indices, K, x)  # numba JIT outside the timing
-    threads = 1
-    if numba is not None:  # pick the fastest thread count (oversubscribed hosts spin badly)
-        best = None
-        cands = sorted({t for t in (1, 2, 4, 8, 16, 32, 64, 128) if t <= os.cpu_count()} | {os.cpu_count()})
-        for th in cands:
-            numba.set_num_threads(min(th, numba.config.NUMBA_NUM_THREADS))
-            orc.csr_matvec(prob.indptr, prob.indices, K, x)
-            t0 = time.perf_counter()
-            for _ in range(5):
-                orc.csr_matvec(prob.indptr, prob.indices, K, x)
-            dt = time.perf_counter() - t0
-            if best is None or dt < best[0]:
-                best = (dt, th)
-        threads = best[1]
-        numba.set_num_threads(min(threads, numba.config.NUMBA_NUM_THREADS))
+def cpu_reference_sample(n_target, n_csr=64, n_cell=8):
+    """Bounded cpu_baseline of our arm (~20 s): the reference package itself (baseline/_ref),
+    composed to n_target^3 from live phase rates (tools/cpu_reference.py ReferenceComposer)
+    with the Krylov phase measured on a 64^3 full-pattern system and scaled by nnz."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_reference as cr
+
     t0 = time.perf_counter()
-    orc.residual(prob, U0)
-    t_R = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    orc.jacobian(prob, U0)
-    t_K = time.perf_counter() - t0
-    reps = 20
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        orc.csr_matvec(prob.indptr, prob.indices, K, x)
-    t_mv = (time.perf_counter() - t0) / reps
-    stats = {}
-    t0 = time.perf_counter()
-    _, norms, its = orc.newton(prob, stats=stats)
-    t_newton = time.perf_counter() - t0
-    mv = stats.get("matvecs", 0)
-    t_vec = max(t_newton - (len(norms)) * t_R - its * t_K - mv * t_mv, 0.0)  # BiCGSTAB vector work
-    ne_s, nnz_s, n_dofs_s = cells.shape[0], prob.indices.size, prob.n_dofs
-    ne_t = n_target ** 3
-    nnz_t = 9 * (3 * n_target + 1) ** 3
-    dofs_t = 3 * (n_target + 1) ** 3
-    mv_t = mv * n_target / n_s  # BiCGSTAB iterations grow ~linearly with the mesh edge (SURVEY 3.3)
-    vec_t = t_vec / (mv * n_dofs_s) * mv_t * dofs_t if mv else 0.0
-    est = len(norms) * t_R / ne_s * ne_t + its * t_K / ne_s * ne_t + mv_t * t_mv / nnz_s * nnz_t + vec_t
-    return {
-        "value": est, "unit": UNIT, "cores": threads, "kind": "port",
-        "sample": (f"oracle NH Newton on {n_s}^3 ({n_dofs_s} DOF) in {t_newton:.2f}s: {its} Newton its, "
-                   f"{mv} matvecs; R {t_R / ne_s * 1e6:.1f} us/cell, K {t_K / ne_s * 1e6:.1f} us/cell, "
-                   f"SpMV {nnz_s * 12 / t_mv / 1e9:.1f} GB/s ({threads} thr); extrapolated to {n_target}^3 with "
-                   f"{mv_t:.0f} matvecs (x n/n_s)"),
-        "sample_wall_s": t_newton,
-    }
+    comp = cr.ReferenceComposer(n_target=n_target, n_csr=n_csr, n_cell=n_cell)
+    r = comp.step()
+    info = cr.host_info()
+    return {"value": r["value"], "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": (f"gradfem (baseline/_ref, unmodified) on {info.get('cpu')} x {os.cpu_count()} threads: "
+                       f"Jacobian / residual rates at {n_cell}^3, workspace rate at 24^3, bicgstab_jacobi and "
+                       f"CsrMatrix.matvec on the full {n_csr}^3 pattern (scaled by nnz to {n_target}^3), "
+                       f"{r['krylov_iterations']} Krylov iterations; composed estimate (DESIGN.md section 4)"),
+            "parts_s": r["parts"], "sample_wall_s": time.perf_counter() - t0}
 
 
 # ----------------------------------------------------------------------- clocks sampler
@@ -471,8 +422,7 @@ def run_ours(args):
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(args.cpu_sample_n, n, s).items()
-                               if k != "sample_wall_s"}
+        out["cpu_baseline"] = cpu_reference_sample(n)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist is not None:
@@ -480,25 +430,44 @@ def run_ours(args):
 
 
 def run_reference(args):
+    """The reference arm: the UNMODIFIED reference package (pip-installed into baseline/_ref)
+    timed on this host's cores, composed to the config-3 solve (tools/cpu_reference.py
+    ReferenceComposer: every phase rate measured live each step; the full-pattern 136^3 system
+    for the Krylov phase).  Rank 0 only; other ranks exit 0."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, walls = [], []
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_reference as cr
+
+    t0 = time.perf_counter()
+    comp = cr.ReferenceComposer(n_target=args.n, n_csr=args.n, n_cell=args.ref_cell_n)
+    setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        cpu_reference_sample(args.cpu_sample_n, args.n, args.stretch)
-    last = None
+        comp.step()
+    vals, walls, last = [], [], None
     for _ in range(args.steps):
-        last = cpu_reference_sample(args.cpu_sample_n, args.n, args.stretch)
+        t0 = time.perf_counter()
+        last = comp.step()
+        walls.append(time.perf_counter() - t0)
         vals.append(last["value"])
-        walls.append(last["sample_wall_s"])
-    v = float(np.mean(vals))
+    v = float(np.median(vals))
+    info = cr.host_info()
+    sample = (f"gradfem (baseline/_ref, unmodified) on {info.get('cpu')} x {os.cpu_count()} threads "
+              f"(numba; OPENBLAS_NUM_THREADS=1): per step assemble_jacobian + assemble_residual at "
+              f"{args.ref_cell_n}^3 and 4 CsrMatrix.matvec on the full {args.n}^3 pattern; setup once: workspace() "
+              f"rate at 24^3, bicgstab_jacobi fixed + per-iteration cost on the full pattern; composed to "
+              f"{args.n}^3 with {last['krylov_iterations']} Krylov iterations ({last['krylov_iterations_source']}), "
+              f"3 Jacobians, 4 residuals (DESIGN.md section 4)")
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(walls)) * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config(args.n, args.stretch),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
-                         "sample": last["sample"]},
+        "data": "synthetic", "config": dict(config(args.n, args.stretch), parallelism="host CPU"),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                         "sample": sample, "estimate": "composed from live phase rates",
+                         "parts_s": last["parts"], "rates": last["rates"], "setup_wall_s": setup_s,
+                         "step_values_s": vals},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

@@ -74,6 +74,32 @@ static double unord_bits(unsigned long long u) {
   return d;
 }
 
+// The same with the point's dphi table in shared memory (dNq[k*3 + d]): lanes of one warp
+// working on different Gauss points would serialise on divergent __constant__ addresses.
+__device__ __forceinline__ double qp_geometry_s(const double (*X)[3], const double *dNq, double (&G)[8][3]) {
+  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) J[a][b] = fma(X[k][a], dNq[k * 3 + b], J[a][b]);
+  const double a = J[0][0], b = J[0][1], c = J[0][2], d = J[1][0], e = J[1][1], f = J[1][2], g = J[2][0],
+               h = J[2][1], i = J[2][2];
+  const double A = e * i - f * h, B = c * h - b * i, C = b * f - c * e;
+  const double D = f * g - d * i, E = a * i - c * g, F = c * d - a * f;
+  const double Gc = d * h - e * g, H = b * g - a * h, I = a * e - b * d;
+  const double det = a * A + b * D + c * Gc;
+  const double r = 1.0 / det;
+  const double inv[3][3] = {{A * r, B * r, C * r}, {D * r, E * r, F * r}, {Gc * r, H * r, I * r}};
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int aa = 0; aa < 3; ++aa)
+      G[k][aa] = inv[0][aa] * dNq[k * 3] + inv[1][aa] * dNq[k * 3 + 1] + inv[2][aa] * dNq[k * 3 + 2];
+  return det;
+}
+
 // J = sum_k X_k (x) dphi_k, cofactor inverse, G_k = J^-T dphi_k (elements.py:117-131)
 __device__ __forceinline__ double qp_geometry(const double (*X)[3], int q, double (&G)[8][3]) {
   double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -154,7 +180,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_residual(ElemArgs a, int64_t n,
   __shared__ double sX[kWarps][4][8][3];
   __shared__ double sU[kWarps][4][8][VEC];
   __shared__ double sT[kWarps][4][8];
+  __shared__ double sdN[8 * 25];  // [q][k*3 + d], point stride 25 (odd: conflict-free)
+  for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
+  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, slot = lane >> 3, q = lane & 7;
+  const double *dNq = sdN + q * 25;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
@@ -169,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_residual(ElemArgs a, int64_t n,
     if (MAT == B200FEM_MAT_POISSON && a.mp.design_source) sT[w][slot][q] = a.theta[node];
     __syncwarp();
     double G[8][3];
-    const double jxw = qp_geometry(sX[w][slot], q, G);
+    const double jxw = qp_geometry_s(sX[w][slot], dNq, G);
     double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
 #pragma unroll
     for (int k = 0; k < 8; ++k)

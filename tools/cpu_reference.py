@@ -219,3 +219,151 @@ if __name__ == "__main__":
         port136(int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 136)
     else:
         raise SystemExit(__doc__)
+
+
+def lattice_csr(n, seed=0):
+    """CSR of a vec-3 operator with the exact pattern the reference builds for an n^3 box mesh
+    (sparse.py:75-108: node blocks of the 27-point lattice stencil, columns ascending), with
+    diagonally dominant values (|off-diagonal row sum| < diagonal): a full-size system on which
+    the reference's own Krylov code (CsrMatrix.matvec -> numba csr_matvec, bicgstab_jacobi) can
+    be timed in seconds, without its ~5 min / 65 GB workspace build."""
+    N1 = n + 1
+    ii, jj = np.meshgrid(np.arange(N1), np.arange(N1), indexing="xy")
+    ii, jj = ii.ravel(), jj.ravel()
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]  # ascending node id
+    indptr_parts, cols, pself = [], [], []
+    for k in range(N1):
+        M = np.full((ii.size, 27), -1, dtype=np.int64)
+        for t, (di, dj, dk) in enumerate(offs):
+            i2, j2, k2 = ii + di, jj + dj, k + dk
+            ok = (i2 >= 0) & (i2 < N1) & (j2 >= 0) & (j2 < N1) & (0 <= k2 < N1)
+            M[ok, t] = i2[ok] + N1 * j2[ok] + N1 * N1 * k2
+        valid = M >= 0
+        cnt = valid.sum(axis=1)
+        pself.append(valid[:, :13].sum(axis=1))
+        indptr_parts.append(np.repeat(3 * cnt, 3))
+        c3 = (3 * M[:, None, :, None] + np.arange(3)[None, None, None, :]).astype(np.int32)
+        cols.append(np.broadcast_to(c3, (ii.size, 3, 27, 3))[np.broadcast_to(valid[:, None, :, None],
+                                                                              (ii.size, 3, 27, 3))])
+    indptr = np.zeros(3 * N1 ** 3 + 1, dtype=np.int64)
+    np.cumsum(np.concatenate(indptr_parts), out=indptr[1:])
+    indices = np.concatenate(cols)
+    del cols
+    data = np.random.default_rng(seed).uniform(-0.012, 0.0, indices.size)
+    ps = np.concatenate(pself)
+    rows = np.arange(3 * N1 ** 3)
+    diag_pos = indptr[:-1] + 3 * np.repeat(ps, 3) + (rows % 3)
+    data[diag_pos] = 1.0
+    return indptr.astype(np.int32), indices, data
+
+
+def reference_krylov_rates(gf, A, iters=(1, 5)):
+    from gradfem.solvers import LinearSolverError
+
+    """Wall time of the reference's bicgstab_jacobi on A at two iteration caps (each raises
+    LinearSolverError at max_iters, after its explicit-residual check): per-iteration cost and
+    the per-solve fixed cost (diagonal() + explicit residuals), plus one CsrMatrix.matvec."""
+    b = np.ones(A.shape[0])
+    x = A.matvec(b)  # numba JIT outside the timing
+    t0 = time.perf_counter()
+    A.matvec(b)
+    t_mv = time.perf_counter() - t0
+    ts = []
+    for k in iters:
+        t0 = time.perf_counter()
+        try:
+            gf.bicgstab_jacobi(A, b, cfg=gf.LinearSolveConfig(rel_tol=1e-300, abs_tol=1e-300, max_iters=k))
+        except LinearSolverError:
+            pass
+        ts.append(time.perf_counter() - t0)
+    per_it = (ts[1] - ts[0]) / (iters[1] - iters[0])
+    return {"matvec_s": t_mv, "bicgstab_iter_s": per_it, "bicgstab_fixed_s": ts[0] - iters[0] * per_it,
+            "raw": dict(zip(iters, ts)), "x_norm": float(np.linalg.norm(x))}
+
+
+# ---------------------------------------------------------------- composed full-size estimate
+C3_KRYLOV_ITERATIONS = 1763   # BiCGSTAB iterations of the config-3 Newton solve (3 solves; the B200
+C3_NEWTON_SOLVES = 3          # run of the same algorithm, BENCH_r01.json; the port's CPU run at full
+C3_RESIDUALS = 4              # size: profiles/r02_port136.json) and Newton residual evaluations
+
+
+def measured_port_iterations():
+    """Krylov iterations of the oracle port's full-size config-3 solve, if measured (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_port136.json")) as fh:
+            d = json.load(fh)
+        return int(d["port"]["krylov_iterations"]), "oracle port at 136^3 on the GPU box host (profiles/r02_port136.json)"
+    except Exception:
+        return C3_KRYLOV_ITERATIONS, "B200 solve of the same algorithm (BENCH_r01.json)"
+
+
+class ReferenceComposer:
+    """Wall time of the reference package's config-3 newton_solve at n_target^3, composed from
+    phases of the UNMODIFIED reference (baseline/_ref) timed live on this host:
+
+      setup    gradfem workspace() at n_ws^3, per cell  x N_e             (assembly.py:83-145)
+      K        gradfem assemble_jacobian at n_cell^3, per cell x N_e      x 3 Newton solves
+      R        gradfem assemble_residual at n_cell^3, per cell x N_e      x 4 evaluations
+      Krylov   gradfem bicgstab_jacobi / CsrMatrix.matvec on a full-pattern n_csr^3 system
+               (the reference's exact sparsity, sparse.py:75-108; scaled by nnz when n_csr <
+               n_target): per-solve fixed cost (diagonal(), explicit residuals) x 3 + per-
+               iteration cost x the config-3 iteration count.
+    The Jacobian/residual are per-cell numpy work (chunks of 1024/8192 cells, assembly.py:28-29)
+    and the matvec is memory-bound, so the per-unit rates transfer; profiles/r02_cpu_ladder.json
+    holds full measured solves at 16^3-64^3 that validate the composition."""
+
+    def __init__(self, n_target=136, n_csr=136, n_cell=10, n_ws=24):
+        self.gf = import_gradfem()
+        self.gf.backend.set_num_threads(os.cpu_count())
+        import fullsize_cases as fc
+        from gradfem.assembly import workspace
+        from gradfem.sparse import CsrMatrix
+
+        self.fc, self.n_target, self.n_csr, self.n_cell = fc, n_target, n_csr, n_cell
+        t0 = time.perf_counter()
+        workspace(fc.c3(self.gf, n_ws))
+        self.ws_per_cell = (time.perf_counter() - t0) / n_ws ** 3
+        self.prob = fc.c3(self.gf, n_cell)
+        workspace(self.prob)
+        self.U = 1e-4 * np.random.default_rng(1).standard_normal(self.prob.n_dofs)
+        self.gf.assemble_jacobian(self.prob, self.U)  # numba / first-call costs outside the steps
+        ip, ix, d = lattice_csr(n_csr)
+        self.A = CsrMatrix(ip, ix, d)
+        self.kry = reference_krylov_rates(self.gf, self.A)
+        self.b = np.ones(self.A.shape[0])
+        self.its, self.its_src = measured_port_iterations()
+
+    def step(self):
+        """One bounded live sample (~seconds): K and R at n_cell^3, four full-pattern matvecs."""
+        gf, N_e = self.gf, self.n_cell ** 3
+        t0 = time.perf_counter()
+        gf.assemble_jacobian(self.prob, self.U)
+        t_K = (time.perf_counter() - t0) / N_e
+        t0 = time.perf_counter()
+        gf.assemble_residual(self.prob, self.U)
+        t_R = (time.perf_counter() - t0) / N_e
+        t0 = time.perf_counter()
+        for _ in range(4):
+            self.A.matvec(self.b)
+        t_mv = (time.perf_counter() - t0) / 4
+        return self.compose(t_K, t_R, t_mv)
+
+    def compose(self, t_K, t_R, t_mv):
+        n = self.n_target
+        Ne = n ** 3
+        scale = 9 * (3 * n + 1) ** 3 / (9 * (3 * self.n_csr + 1) ** 3)  # nnz ratio
+        k = self.kry
+        t_vec = max(k["bicgstab_iter_s"] - 2 * k["matvec_s"], 0.0)  # BiCGSTAB vector work per iteration
+        t_iter = (2 * t_mv + t_vec) * scale
+        # BiCGSTAB iterations grow ~linearly with the mesh edge (SURVEY.md 3.3) for other sizes
+        its = self.its if n == 136 else self.its * n / 136.0
+        parts = {"setup_s": self.ws_per_cell * Ne, "jacobian_s": C3_NEWTON_SOLVES * t_K * Ne,
+                 "residual_s": C3_RESIDUALS * t_R * Ne,
+                 "krylov_s": C3_NEWTON_SOLVES * k["bicgstab_fixed_s"] * scale + its * t_iter}
+        return {"value": sum(parts.values()), "parts": parts,
+                "rates": {"jacobian_us_per_cell": t_K * 1e6, "residual_us_per_cell": t_R * 1e6,
+                          "matvec_s_at_n_csr": t_mv, "matvec_gbs": 12 * self.A.nnz / t_mv / 1e9,
+                          "bicgstab_iter_s_at_target": t_iter,
+                          "bicgstab_fixed_s_at_n_csr": k["bicgstab_fixed_s"],
+                          "workspace_us_per_cell": self.ws_per_cell * 1e6},
+                "krylov_iterations": its, "krylov_iterations_source": self.its_src}
