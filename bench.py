@@ -285,6 +285,18 @@ def run_ours(args):
     t_spmv = e0.elapsed_time(e1) / reps / 1e3
     from paper_2212_00964_b200.sparse import GridOperator
     grid_op = isinstance(K, GridOperator)
+    # one BiCGSTAB iteration inside the while-graph vs its kernels timed one by one
+    kprof = None
+    if part is None:
+        import ctypes as C
+
+        prof = (C.c_double * 8)()
+        xb = D.empty(Nl)
+        if lib.b200fem_bicgstab_profile(h, D.ptr(x), D.ptr(xb), 60, prof) == 0:
+            names = ["update_p", "spmv_jacobi_r0", "update_s", "spmv_jacobi_tt", "update_xr", "loop_cond"]
+            kprof = {"graph_iter_us": prof[0], "kernels_us": dict(zip(names, prof[1:7])), "kernel_sum_us": prof[7],
+                     "gap_us": prof[0] - prof[7], "iterations": 60}
+        del xb
     ip = ws.indptr
     nnz_rows = int(ip[3 * (row_lo + n_rows_nodes)] - ip[3 * row_lo])
     rows = 3 * n_rows_nodes
@@ -402,6 +414,7 @@ def run_ours(args):
                    "phase_s": getattr(rep, "timings", None),
                    "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
                    "in_solve_iter_ms": in_solve_iter_ms, "per_step_ms": per_step},
+        "krylov_profile": kprof,
         "alt_linear": alt,
         "alt_mixed_precision": mixed,
         "assembly": {"residual_ms": t_res * 1e3, "residual_mcells_s": n_cells_l / t_res / 1e6,

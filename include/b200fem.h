@@ -213,6 +213,11 @@ int b200fem_bicgstab(b200fem_matrix *m, const double *b_dev, double *x_dev, int3
  * config 2).  FEM matrices: starts from x_d = b_d on Dirichlet rows so the row-replaced K
  * acts as its SPD free block.  Same termination rule as bicgstab (true residual); restarts
  * from the explicit residual; BreakdownError if p.Ap <= 0. */
+/* diagnostics: one BiCGSTAB iteration as run inside the while-graph (out_us[0], over `iters`
+ * iterations from x = 0 with tolerance 0) against its kernels timed one by one (out_us[1..6]:
+ * update_p, SpMV r0.v, update_s, SpMV t.t/t.s, update_xr, loop condition; out_us[7] = sum).
+ * Overwrites x; b is the right-hand side. */
+int b200fem_bicgstab_profile(b200fem_matrix *m, const double *b_dev, double *x_dev, int32_t iters, double *out_us);
 int b200fem_pcg(b200fem_matrix *m, const double *b_dev, double *x_dev, int32_t has_x0, double rel_tol,
                 double abs_tol, int64_t max_iters, b200fem_solve_info *info, b200fem_error *err);
 

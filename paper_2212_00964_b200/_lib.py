@@ -98,6 +98,7 @@ SIGNATURES = {
     "b200fem_matvec": (C.c_int, [_vp, _vp, _vp]),
     "b200fem_diagonal": (C.c_int, [_vp, _vp]),
     "b200fem_bicgstab": (C.c_int, [_vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo), _perr]),
+    "b200fem_bicgstab_profile": (C.c_int, [_vp, _vp, _vp, _i32, _pf64]),
     "b200fem_pcg": (C.c_int, [_vp, _vp, _vp, _i32, _f64, _f64, _i64, C.POINTER(SolveInfo), _perr]),
     "b200fem_comm_unique_id": (C.c_int, [_vp]),
     "b200fem_comm_create_nccl": (C.c_int, [C.POINTER(_vp), _vp, _i32, _i32]),

@@ -150,6 +150,10 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const KrylovScalars *S
   cudaGraphSetConditional(h, S->status == KS_RUNNING ? 1u : 0u);
 }
 
+__global__ void k_loop_status(const KrylovScalars *S) {
+  if (S->status == 12345) __trap();  // same single-thread read of the status as k_loop_cond
+}
+
 static bool use_graph_loop() {
   static int v = -1;
   if (v < 0) v = getenv("B200FEM_NO_GRAPH") ? 0 : 1;
@@ -238,6 +242,83 @@ static void enqueue_iteration(Matrix *m, const double *b, double *x) {
   k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
   count_launch(3);
   (void)b;
+}
+
+// Diagnostics (bench.py "krylov_profile"): one BiCGSTAB iteration of `m` as it runs inside the
+// while-graph, against its kernels timed one by one (CUDA events on the matrix's stream).
+// out_us[0] = graph-loop time per iteration (`iters` iterations, tolerance 0), out_us[1..6] =
+// k_update_p, SpMV (v = D^-1 A p, r0.v), k_update_s, SpMV (t = D^-1 A s, t.t, t.s),
+// k_update_xr, k_loop_cond, each averaged over `iters` back-to-back launches; out_us[7] = sum.
+static int bicgstab_profile(Matrix *m, const double *b, double *x, int iters, double *out_us) {
+  if (ensure_work(m)) return B200FEM_E_CUDA;
+  KrylovWork *w = m->kw;
+  cudaStream_t s = m->stream;
+  const int64_t n = m->n;
+  int64_t nz = 0;
+  if (launch_diagonal(m, w->diag, w->inv, &w->red, &nz) || nz) return B200FEM_E_INVALID;
+  B200_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  KrylovScalars H{};
+  H.status = KS_RUNNING;
+  H.first = 1;
+  H.rho = H.alpha = H.omega = 1.0;
+  H.tol = 0.0;
+  H.max_iters = iters;
+  B200_CUDA(cudaMemcpyAsync(w->sc, &H, sizeof(H), cudaMemcpyHostToDevice, s));
+  SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->r0, w->sc, 1};
+  if (launch_spmv(m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
+  B200_CUDA(cudaMemsetAsync(w->v, 0, n * sizeof(double), s));
+  B200_CUDA(cudaMemsetAsync(w->p, 0, n * sizeof(double), s));
+  k_begin<<<1, 1, 0, s>>>(w->sc);
+  cudaEvent_t e0, e1;
+  B200_CUDA(cudaEventCreate(&e0));
+  B200_CUDA(cudaEventCreate(&e1));
+  int rc = 0;
+  {
+    LoopGraph lg;
+    b200fem_error err{};
+    B200_CUDA(cudaEventRecord(e0, s));
+    rc = run_loop_graph(m, lg, [&] { enqueue_iteration(m, b, x); }, &err);
+    B200_CUDA(cudaEventRecord(e1, s));
+    B200_CUDA(cudaEventSynchronize(e1));
+  }
+  KrylovScalars done{};
+  B200_CUDA(cudaMemcpy(&done, w->sc, sizeof(done), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  out_us[0] = 1e3 * ms / std::max<long long>(done.it, 1);
+  // kernels one at a time (status forced RUNNING, no iteration cap)
+  H = done;
+  H.status = KS_RUNNING;
+  H.max_iters = 1ll << 60;
+  B200_CUDA(cudaMemcpyAsync(w->sc, &H, sizeof(H), cudaMemcpyHostToDevice, s));
+  SpmvArgs a1{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 1};
+  SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 1};
+  for (int k = 1; k <= 6 && !rc; ++k) {
+    B200_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) {
+      switch (k) {
+        case 1: k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc); break;
+        case 2: rc |= launch_spmv(m, SP_JACOBI_R0, a1, &w->red); break;
+        case 3: k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc); break;
+        case 4: rc |= launch_spmv(m, SP_JACOBI_TT, a2, &w->red); break;
+        case 5:
+          k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
+          break;
+        default: k_loop_status<<<1, 1, 0, s>>>(w->sc); break;
+      }
+    }
+    B200_CUDA(cudaEventRecord(e1, s));
+    B200_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    out_us[k] = 1e3 * ms / iters;
+    // keep the recurrence alive (a breakdown would gate the kernels off)
+    B200_CUDA(cudaMemcpyAsync(w->sc, &H, sizeof(H), cudaMemcpyHostToDevice, s));
+  }
+  out_us[7] = out_us[1] + out_us[2] + out_us[3] + out_us[4] + out_us[5] + out_us[6];
+  count_launch(6 * iters + 2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc ? B200FEM_E_CUDA : 0;
 }
 
 int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol, int64_t max_iters,
@@ -680,6 +761,12 @@ int b200fem_bicgstab(b200fem_matrix *mm, const double *b, double *x, int32_t has
     return 0;
   }
   return bicgstab(m, b, x, has_x0, rel_tol, abs_tol, max_iters, info, err);
+}
+
+int b200fem_bicgstab_profile(b200fem_matrix *mm, const double *b, double *x, int32_t iters, double *out_us) {
+  Matrix *m = (Matrix *)mm;
+  if (!m || !b || !x || !out_us || iters < 1) return B200FEM_E_INVALID;
+  return bicgstab_profile(m, b, x, iters, out_us);
 }
 
 }  // extern "C"
