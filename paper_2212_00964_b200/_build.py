@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", INCLUDE]
-SOURCES = ["context.cu", "element.cu", "material.cu", "spmv.cu", "krylov.cu", "krylov_dist.cu", "transpose.cu", "design.cu", "io.cu", "lowseam.cu"]
+SOURCES = ["context.cu", "element.cu", "material.cu", "spmv.cu", "spmv_alt.cu", "krylov.cu", "krylov_dist.cu", "transpose.cu", "design.cu", "io.cu", "lowseam.cu"]
 
 
 def _deps():

@@ -1730,13 +1730,15 @@ static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, dou
   k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
 }
 
-// B200FEM_TANGENT = v1 (pair-per-lane phase A) | v2 (node-lane phase A) | fused (lattice column
-// kernel for the GRID3 tangent; v2 elsewhere).  Read once per process.
+// B200FEM_TANGENT = v2 (default: node-lane phase A) | v1 (pair-per-lane phase A) | fused
+// (lattice column kernel for the GRID3 tangent, v2 elsewhere: correct, but one 200 KB CTA of 4
+// warps per SM leaves it latency bound -- 16.0 ms against 8.4 ms for v2 + pull at config 3,
+// profiles/r02_tangent_ab.jsonl).  Read once per process.
 static int tangent_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("B200FEM_TANGENT");
-    v = !e ? 0 : !strcmp(e, "v2") ? 1 : !strcmp(e, "fused") ? 2 : 0;
+    v = !e ? 1 : !strcmp(e, "v1") ? 0 : !strcmp(e, "fused") ? 2 : 1;
   }
   return v;
 }

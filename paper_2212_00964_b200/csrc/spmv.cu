@@ -22,104 +22,10 @@
 #include <cstring>
 
 #include "internal.cuh"
+#include "spmv_common.cuh"
 
 namespace b200 {
 
-// Row operands the epilogue needs, loaded at the START of a row's work so their latency
-// overlaps the value stream instead of serialising after the reduction.
-struct RowPre {
-  double inv, aux, dg, xi;
-};
-
-template <int MODE>
-__device__ __forceinline__ RowPre spmv_preload(int64_t i, const SpmvArgs &a) {
-  RowPre p{0.0, 0.0, 0.0, 0.0};
-  if (MODE == SP_JACOBI_R0) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
-  } else if (MODE == SP_JACOBI_TT) {
-    p.inv = __ldg(a.inv + i);
-    p.xi = __ldg(a.x + i);
-  } else if (MODE == SP_RESIDUAL) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
-    p.dg = __ldg(a.dg + i);
-  } else if (MODE == SP_PQ) {
-    p.xi = __ldg(a.x + i);
-  } else if (MODE == SP_CGRES) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
-  }
-  return p;
-}
-
-// Post-process row i's dot-product value `acc` for the mode; accumulate reduction terms.
-template <int MODE>
-__device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvArgs &a, const RowPre &p,
-                                              double &red0, double &red1) {
-  if (MODE == SP_PLAIN) {
-    a.y[i] = acc;
-  } else if (MODE == SP_JACOBI_R0) {
-    const double v = p.inv * acc;
-    a.y[i] = v;
-    red0 = fma(p.aux, v, red0);
-  } else if (MODE == SP_JACOBI_TT) {
-    const double t = p.inv * acc;
-    a.y[i] = t;
-    red0 = fma(t, t, red0);
-    red1 = fma(t, p.xi, red1);
-  } else if (MODE == SP_RESIDUAL) {
-    const double r = p.inv * (p.aux - acc);
-    a.y[i] = r;
-    a.aux2[i] = r;
-    const double dr = p.dg * r;
-    red0 = fma(dr, dr, red0);
-    red1 = fma(r, r, red1);
-  } else if (MODE == SP_PQ) {  // q = A p, p.q
-    a.y[i] = acc;
-    red0 = fma(p.xi, acc, red0);
-  } else {  // SP_CGRES: r = b - A x, p = z = D^-1 r, ||r||^2, r.z
-    const double r = p.aux - acc;
-    const double z = p.inv * r;
-    a.y[i] = r;
-    a.aux2[i] = z;
-    red0 = fma(r, r, red0);
-    red1 = fma(r, z, red1);
-  }
-}
-
-// Scalar updates performed by the last block of a reduction launch (one rank).
-template <int MODE>
-__device__ __forceinline__ void spmv_stage(KrylovScalars *S, const double (&tot)[2]) {
-  if (MODE == SP_JACOBI_R0) apply_stage(ST_R0, S, tot);
-  else if (MODE == SP_JACOBI_TT) apply_stage(ST_TT, S, tot);
-  else if (MODE == SP_RESIDUAL) apply_stage(ST_RES, S, tot);
-  else if (MODE == SP_PQ) apply_stage(ST_PQ, S, tot);
-  else if (MODE == SP_CGRES) apply_stage(ST_CGRES, S, tot);
-}
-
-// Sum three per-lane partials over the warp with a reduce-scatter (6 double shuffles
-// instead of 3 full butterflies = 15): afterwards lane 0 holds row 0, lane 8 row 1,
-// lane 16 row 2.  Fixed tree -> deterministic.
-__device__ __forceinline__ double warp_sum3(double y0, double y1, double y2, int lane) {
-  const bool h4 = lane & 16;
-  const double s0 = h4 ? y0 : y2, s1 = h4 ? y1 : 0.0;
-  double k0 = (h4 ? y2 : y0) + __shfl_xor_sync(0xffffffffu, s0, 16);
-  double k1 = (h4 ? 0.0 : y1) + __shfl_xor_sync(0xffffffffu, s1, 16);
-  const bool h3 = lane & 8;
-  double kk = (h3 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8);
-  kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-  kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-  kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-  return kk;
-}
-
-// Warp per node, lane per neighbour node j: the lane loads x_m (3 doubles, L2-resident)
-// once and the 3x3 block of values A[3n+c, 3m+k] from the three contiguous row segments
-// (rows are 3*cnt long; lane j's entries sit at 3j..3j+2 of each row, so a warp load
-// instruction covers one row's 27*24 B contiguous span).  12 independent loads per lane,
-// ~60 warp instructions per node; values are streamed with an evict-first hint so x stays
-// in L2; the 3 row sums use a 6-shuffle reduce-scatter.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 4) k_spmv_fem3(const int32_t *__restrict__ nbr_ptr,
                                                         const int32_t *__restrict__ nbr,
@@ -239,241 +145,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_sym3(const int32_t *__rest
     double v2[2] = {red0, red1}, tot[2];
     if (block_partials_and_finish<2>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage) spmv_stage<MODE>(a.sc, tot);
   }
-}
-
-// ------------------------------------------------------------------------------------
-// FEM3 SpMV, Blackwell bulk-copy pipeline.  One persistent 1024-thread CTA per SM: a
-// producer lane streams contiguous node chunks (their CSR values and neighbour lists are
-// contiguous in memory for consecutive nodes) into a 3-stage shared-memory ring with
-// cp.async.bulk + mbarrier complete_tx; 31 consumer warps take one node each per chunk,
-// gather x from L2 and read the values from shared memory.  The copy engine keeps up to
-// two 60 KB chunks per SM in flight without spending registers.  Same per-lane arithmetic
-// and reduction tree as k_spmv_fem3 -> bit-identical y.
-constexpr int kTmaConsumers = 31;
-constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
-constexpr int kTmaStages = 3;
-constexpr int kTmaValBytes = 62 * 1024;
-constexpr int kTmaNbrBytes = 4096;
-constexpr int kTmaExtBytes = 768;  // one row-operand array of a chunk (<= 93 rows + alignment slack)
-constexpr int kTmaStageBytes = kTmaValBytes + kTmaNbrBytes + 3 * kTmaExtBytes;
-constexpr int kTmaSmem = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-constexpr uint32_t kMbarSuspendNs = 20000;
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  uint32_t ok = 0;
-  do {  // suspend-time hint: a waiting warp sleeps instead of re-polling (issue slots, power)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity), "r"(kMbarSuspendNs)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-// Row operands of the epilogue, streamed into the stage with the values (so the row lanes
-// read them from shared memory instead of issuing scattered 8-byte loads).
-template <int MODE>
-__host__ __device__ constexpr int n_ext() {
-  return MODE == SP_JACOBI_R0 ? 2 : MODE == SP_JACOBI_TT ? 2 : MODE == SP_RESIDUAL ? 3 : MODE == SP_PQ ? 1
-       : MODE == SP_CGRES ? 2 : 0;
-}
-template <int MODE>
-__device__ __forceinline__ const double *ext_ptr(const SpmvArgs &a, int k) {
-  if (MODE == SP_JACOBI_R0) return k == 0 ? a.inv : a.aux;
-  if (MODE == SP_JACOBI_TT) return k == 0 ? a.inv : a.x;
-  if (MODE == SP_RESIDUAL) return k == 0 ? a.inv : (k == 1 ? a.aux : a.dg);
-  if (MODE == SP_PQ) return a.x;
-  return k == 0 ? a.inv : a.aux;  // SP_CGRES
-}
-template <int MODE>
-__device__ __forceinline__ RowPre row_pre_from(const double *e0, const double *e1, const double *e2) {
-  RowPre p{0.0, 0.0, 0.0, 0.0};
-  if (MODE == SP_JACOBI_R0) p.inv = *e0, p.aux = *e1;
-  else if (MODE == SP_JACOBI_TT) p.inv = *e0, p.xi = *e1;
-  else if (MODE == SP_RESIDUAL) p.inv = *e0, p.aux = *e1, p.dg = *e2;
-  else if (MODE == SP_PQ) p.xi = *e0;
-  else if (MODE == SP_CGRES) p.inv = *e0, p.aux = *e1;
-  return p;
-}
-
-// x_m of neighbour node m (3 doubles at 24 m).  XV=0: three 8-byte loads; XV=1: one
-// 16-byte load of the aligned pair plus one 8-byte load (x must be 16-byte aligned);
-// XV=2 (diagnostic only, wrong results): no gather, to separate its cost.
-template <int XV>
-__device__ __forceinline__ void load_x3(const double *__restrict__ x, int m, double &x0, double &x1, double &x2) {
-  const double *__restrict__ xm = x + 3 * (int64_t)m;
-  if (XV == 0) {
-    x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
-  } else if (XV == 1) {
-    const int odd = m & 1;
-    const double2 v = __ldg(reinterpret_cast<const double2 *>(xm + odd));
-    const double sc = __ldg(xm + (odd ? 0 : 2));
-    x0 = odd ? sc : v.x;
-    x1 = odd ? v.x : v.y;
-    x2 = odd ? v.y : sc;
-  } else {
-    x0 = 1.0, x1 = 0.5, x2 = 0.25;
-  }
-}
-
-// One node's three row sums from a value block `sv` (stage or global) and its neighbour ids.
-template <int XV = 0>
-__device__ __forceinline__ void node_rows(const double *sv, const int32_t *sn, int cnt, const double *__restrict__ x,
-                                          int lane, double &y0, double &y1, double &y2) {
-  const int L = 3 * cnt;
-  for (int j = lane; j < cnt; j += 32) {
-    const int m = sn[j];
-    double x0, x1, x2;
-    load_x3<XV>(x, m, x0, x1, x2);
-    const double *r0 = sv + 3 * j;
-    y0 = fma(r0[2], x2, fma(r0[1], x1, fma(r0[0], x0, y0)));
-    y1 = fma(r0[L + 2], x2, fma(r0[L + 1], x1, fma(r0[L], x0, y1)));
-    y2 = fma(r0[2 * L + 2], x2, fma(r0[2 * L + 1], x1, fma(r0[2 * L], x0, y2)));
-  }
-}
-
-template <int MODE, int XV>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_fem3_tma(const int32_t *__restrict__ nbr_ptr,
-                                                                 const int32_t *__restrict__ nbr,
-                                                                 const double *__restrict__ data,
-                                                                 const int32_t *__restrict__ chunk_node, int n_chunks,
-                                                                 int64_t total_blocks, int64_t n_rows, SpmvArgs a,
-                                                                 RedScratch red) {
-  if (a.sc && a.sc->status != KS_RUNNING) return;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kTmaStageBytes);
-  uint64_t *empty = full + kTmaStages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kTmaConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // the last chunk's end may not be 16-byte aligned: it is read from global memory instead
-  const uint64_t val_end = (uint64_t)total_blocks * 72, nbr_end = (uint64_t)total_blocks * 4;
-  const uint64_t row_end = (uint64_t)n_rows * 8;
-  double red0 = 0.0, red1 = 0.0;
-  if (warp == kTmaConsumers) {
-    if (lane == 0) {  // producer
-      int it = 0;
-      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-        const int s = it % kTmaStages;
-        const uint32_t ph = (it / kTmaStages) & 1;
-        mbar_wait(empty + s, ph ^ 1);
-        const int64_t p0 = __ldg(nbr_ptr + __ldg(chunk_node + c)), p1 = __ldg(nbr_ptr + __ldg(chunk_node + c + 1));
-        const uint64_t vb0 = (72ull * p0) & ~15ull, vb1 = std::min((72ull * p1 + 15) & ~15ull, val_end & ~15ull);
-        const uint64_t nb0 = (4ull * p0) & ~15ull, nb1 = std::min((4ull * p1 + 15) & ~15ull, nbr_end & ~15ull);
-        const int64_t cn0 = __ldg(chunk_node + c), cn1 = __ldg(chunk_node + c + 1);
-        const uint64_t eb0 = (24ull * cn0) & ~15ull, eb1 = std::min((24ull * cn1 + 15) & ~15ull, row_end & ~15ull);
-        const uint32_t ext_bytes = eb1 > eb0 ? (uint32_t)(eb1 - eb0) : 0u;
-        mbar_expect_tx(full + s, (uint32_t)((vb1 - vb0) + (nb1 - nb0)) + n_ext<MODE>() * ext_bytes);
-        uint8_t *stage = smem + s * kTmaStageBytes;
-        if (vb1 > vb0) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(data) + vb0, (uint32_t)(vb1 - vb0), full + s);
-        if (nb1 > nb0)
-          bulk_g2s(stage + kTmaValBytes, reinterpret_cast<const uint8_t *>(nbr) + nb0, (uint32_t)(nb1 - nb0), full + s);
-#pragma unroll
-        for (int k = 0; k < n_ext<MODE>(); ++k)
-          if (ext_bytes)
-            bulk_g2s(stage + kTmaValBytes + kTmaNbrBytes + k * kTmaExtBytes,
-                     reinterpret_cast<const uint8_t *>(ext_ptr<MODE>(a, k)) + eb0, ext_bytes, full + s);
-      }
-    }
-    __syncwarp();  // reconverge the producer warp before the block-wide reduction barrier
-  } else {
-    int it = 0;
-    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-      const int s = it % kTmaStages;
-      const uint32_t ph = (it / kTmaStages) & 1;
-      const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
-      const int64_t pc = __ldg(nbr_ptr + n0), pe = __ldg(nbr_ptr + n1);
-      const uint64_t vb0 = (72ull * pc) & ~15ull, nb0 = (4ull * pc) & ~15ull;
-      const bool tail = (72ull * pe > (val_end & ~15ull)) || (4ull * pe > (nbr_end & ~15ull)) ||
-                        (n_ext<MODE>() > 0 && 24ull * n1 > (row_end & ~15ull));
-      const uint64_t eb0 = (24ull * n0) & ~15ull;
-      const uint8_t *stage = smem + s * kTmaStageBytes;
-      const int nA = n0 + warp;
-      const bool has = nA < n1;
-      int64_t pA = 0;
-      int cA = 0;
-      if (has) {
-        pA = __ldg(nbr_ptr + nA);
-        cA = __ldg(nbr_ptr + nA + 1) - (int)pA;
-      }
-      const bool row_lane = (lane & 7) == 0 && lane < 24;
-      const int64_t row = 3 * (int64_t)nA + (lane >> 3);
-      RowPre pre{0.0, 0.0, 0.0, 0.0};
-      if (tail && row_lane && has) pre = spmv_preload<MODE>(row, a);
-      mbar_wait(full + s, ph);
-      if (!tail && row_lane && has && n_ext<MODE>() > 0) {
-        const uint8_t *ext = stage + kTmaValBytes + kTmaNbrBytes + (8ull * row - eb0);
-        pre = row_pre_from<MODE>(reinterpret_cast<const double *>(ext),
-                                 reinterpret_cast<const double *>(ext + kTmaExtBytes),
-                                 reinterpret_cast<const double *>(ext + 2 * kTmaExtBytes));
-      }
-      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-      if (has) {
-        if (!tail)
-          node_rows<XV>(reinterpret_cast<const double *>(stage + (72ull * pA - vb0)),
-                    reinterpret_cast<const int32_t *>(stage + kTmaValBytes + (4ull * pA - nb0)), cA, a.x, lane, y0, y1,
-                    y2);
-        else
-          node_rows<XV>(data + 9 * pA, nbr + pA, cA, a.x, lane, y0, y1, y2);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);  // stage reads done; the producer may refill it
-      if (has) {
-        const double acc = warp_sum3(y0, y1, y2, lane);
-        if (row_lane) spmv_epilogue<MODE>(3 * (int64_t)nA + (lane >> 3), acc, a, pre, red0, red1);
-      }
-    }
-  }
-  if (MODE != SP_PLAIN) {
-    double v2[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
-      spmv_stage<MODE>(a.sc, tot);
-  }
-}
-
-template <int XV>
-static void set_tma_attr() {
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PLAIN, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_R0, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_JACOBI_TT, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_RESIDUAL, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_PQ, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-  cudaFuncSetAttribute(k_spmv_fem3_tma<SP_CGRES, XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
-}
-
-// x-gather variant of the bulk-copy kernel (B200FEM_SPMV_X = "vec" | "none"; "none" is a
-// diagnostic that skips the gather and computes wrong results).
-static int tma_x_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("B200FEM_SPMV_X");
-    v = (e && !strcmp(e, "vec")) ? 1 : (e && !strcmp(e, "none")) ? 2 : 0;
-  }
-  return v;
 }
 
 // Two nodes per consumer warp (half-warp per node, two neighbours per lane): the per-node
@@ -663,192 +334,13 @@ int prepare_fem3_chunks(Matrix *m, int64_t lo, int64_t hi) {
     return B200FEM_E_CUDA;
   static bool attr = false;
   if (!attr) {
-    set_tma_attr<0>();
-    set_tma_attr<1>();
-    set_tma_attr<2>();
+    set_fem3_tma_npw1_attr();  // spmv_alt.cu
     set_t2_attr();
     attr = true;
   }
   m->use_tma = true;
   return 0;
 }
-
-// ------------------------------------------------------------------------------------
-// SYM3 with the bulk-copy pipeline: the chunk's upper blocks, neighbour ids, lower-block
-// indices and row operands are contiguous for consecutive nodes and stream into shared
-// memory; the consumer warps gather only x and the lower blocks (L2-resident: they were
-// streamed as upper blocks of nearby rows moments before).  One memory round trip per node.
-constexpr int kSymUpBytes = 40 * 1024;
-constexpr int kSymNbrBytes = 4096;
-constexpr int kSymStageBytes = kSymUpBytes + 2 * kSymNbrBytes + 3 * kTmaExtBytes;
-constexpr int kSymStages = 4;
-constexpr int kSymSmem = kSymStages * kSymStageBytes + 2 * kSymStages * 8;
-
-template <int MODE>
-__global__ void __launch_bounds__(kTmaThreads, 1) k_spmv_sym3_tma(
-    const int32_t *__restrict__ nbr_ptr, const int32_t *__restrict__ nbr, const int32_t *__restrict__ up_ptr,
-    const int32_t *__restrict__ lo_blk, const double *__restrict__ sym, const uint8_t *__restrict__ dir_flag,
-    const int32_t *__restrict__ chunk_node, int n_chunks, int64_t n_nodes, SpmvArgs a, RedScratch red) {
-  if (a.sc && a.sc->status != KS_RUNNING) return;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSymStages * kSymStageBytes);
-  uint64_t *empty = full + kSymStages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSymStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kTmaConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint64_t up_end = (uint64_t)__ldg(up_ptr + n_nodes) * 72, nb_end = (uint64_t)__ldg(nbr_ptr + n_nodes) * 4;
-  const uint64_t row_end = (uint64_t)n_nodes * 24;
-  double red0 = 0.0, red1 = 0.0;
-  if (warp == kTmaConsumers) {
-    if (lane == 0) {  // producer
-      int it = 0;
-      for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-        const int s = it % kSymStages;
-        const uint32_t ph = (it / kSymStages) & 1;
-        mbar_wait(empty + s, ph ^ 1);
-        const int64_t n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
-        const uint64_t u0 = (72ull * __ldg(up_ptr + n0)) & ~15ull,
-                       u1 = std::min((72ull * __ldg(up_ptr + n1) + 15) & ~15ull, up_end & ~15ull);
-        const uint64_t b0 = (4ull * __ldg(nbr_ptr + n0)) & ~15ull,
-                       b1 = std::min((4ull * __ldg(nbr_ptr + n1) + 15) & ~15ull, nb_end & ~15ull);
-        const uint64_t e0 = (24ull * n0) & ~15ull, e1 = std::min((24ull * n1 + 15) & ~15ull, row_end & ~15ull);
-        const uint32_t ub = u1 > u0 ? (uint32_t)(u1 - u0) : 0u, nb = b1 > b0 ? (uint32_t)(b1 - b0) : 0u,
-                       eb = e1 > e0 ? (uint32_t)(e1 - e0) : 0u;
-        mbar_expect_tx(full + s, ub + 2 * nb + n_ext<MODE>() * eb);
-        uint8_t *stage = smem + s * kSymStageBytes;
-        if (ub) bulk_g2s(stage, reinterpret_cast<const uint8_t *>(sym) + u0, ub, full + s);
-        if (nb) {
-          bulk_g2s(stage + kSymUpBytes, reinterpret_cast<const uint8_t *>(nbr) + b0, nb, full + s);
-          bulk_g2s(stage + kSymUpBytes + kSymNbrBytes, reinterpret_cast<const uint8_t *>(lo_blk) + b0, nb, full + s);
-        }
-#pragma unroll
-        for (int k = 0; k < n_ext<MODE>(); ++k)
-          if (eb)
-            bulk_g2s(stage + kSymUpBytes + 2 * kSymNbrBytes + k * kTmaExtBytes,
-                     reinterpret_cast<const uint8_t *>(ext_ptr<MODE>(a, k)) + e0, eb, full + s);
-      }
-    }
-    __syncwarp();
-  } else {
-    int it = 0;
-    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-      const int s = it % kSymStages;
-      const uint32_t ph = (it / kSymStages) & 1;
-      const int n0 = __ldg(chunk_node + c), n1 = __ldg(chunk_node + c + 1);
-      const int64_t u0 = (72ll * __ldg(up_ptr + n0)) & ~15ll, b0 = (4ll * __ldg(nbr_ptr + n0)) & ~15ll;
-      const uint64_t e0 = (24ull * n0) & ~15ull;
-      const bool tail = (72ull * __ldg(up_ptr + n1) > (up_end & ~15ull)) ||
-                        (4ull * __ldg(nbr_ptr + n1) > (nb_end & ~15ull)) ||
-                        (n_ext<MODE>() > 0 && 24ull * n1 > (row_end & ~15ull));
-      const uint8_t *stage = smem + s * kSymStageBytes;
-      const int n = n0 + warp;
-      const bool has = n < n1;
-      int p0 = 0, cnt = 0, ubn = 0, self = 0;
-      if (has) {
-        p0 = __ldg(nbr_ptr + n);
-        cnt = __ldg(nbr_ptr + n + 1) - p0;
-        ubn = __ldg(up_ptr + n);
-        self = cnt - (__ldg(up_ptr + n + 1) - ubn);
-      }
-      const bool row_lane = (lane & 7) == 0 && lane < 24;
-      const int64_t row = 3 * (int64_t)n + (lane >> 3);
-      RowPre pre{0.0, 0.0, 0.0, 0.0};
-      bool dflag = false;
-      double xrow = 0.0;
-      if (row_lane && has) {
-        if (tail) pre = spmv_preload<MODE>(row, a);
-        dflag = dir_flag && __ldg(dir_flag + row);
-        if (dflag) xrow = __ldg(a.x + row);
-      }
-      mbar_wait(full + s, ph);
-      if (!tail && row_lane && has && n_ext<MODE>() > 0) {
-        const uint8_t *ext = stage + kSymUpBytes + 2 * kSymNbrBytes + (8ull * row - e0);
-        pre = row_pre_from<MODE>(reinterpret_cast<const double *>(ext),
-                                 reinterpret_cast<const double *>(ext + kTmaExtBytes),
-                                 reinterpret_cast<const double *>(ext + 2 * kTmaExtBytes));
-      }
-      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-      if (has) {
-        const int32_t *sn = tail ? nbr + p0 : reinterpret_cast<const int32_t *>(stage + kSymUpBytes + (4ll * p0 - b0));
-        const int32_t *sl =
-            tail ? lo_blk + p0 : reinterpret_cast<const int32_t *>(stage + kSymUpBytes + kSymNbrBytes + (4ll * p0 - b0));
-        const double *su = tail ? sym + 9 * (int64_t)ubn : reinterpret_cast<const double *>(stage + (72ll * ubn - u0));
-        for (int j = lane; j < cnt; j += 32) {
-          const int m = sn[j];
-          const bool lower = j < self;
-          const double *B = lower ? sym + 9 * (int64_t)sl[j] : su + 9 * (j - self);
-          double bb[9];
-#pragma unroll
-          for (int t = 0; t < 9; ++t) bb[t] = lower ? __ldg(B + t) : B[t];
-          const double *__restrict__ xm = a.x + 3 * (int64_t)m;
-          const double x0 = __ldg(xm), x1 = __ldg(xm + 1), x2 = __ldg(xm + 2);
-          const double a01 = lower ? bb[3] : bb[1], a02 = lower ? bb[6] : bb[2], a10 = lower ? bb[1] : bb[3];
-          const double a12 = lower ? bb[7] : bb[5], a20 = lower ? bb[2] : bb[6], a21 = lower ? bb[5] : bb[7];
-          y0 = fma(a02, x2, fma(a01, x1, fma(bb[0], x0, y0)));
-          y1 = fma(a12, x2, fma(bb[4], x1, fma(a10, x0, y1)));
-          y2 = fma(bb[8], x2, fma(a21, x1, fma(a20, x0, y2)));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
-      if (has) {
-        double acc = warp_sum3(y0, y1, y2, lane);
-        if (row_lane) {
-          if (dflag) acc = xrow;
-          spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
-        }
-      }
-    }
-  }
-  if (MODE != SP_PLAIN) {
-    double v2[2] = {red0, red1}, tot[2];
-    if (block_partials_and_finish<2, kTmaConsumers + 1>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
-      spmv_stage<MODE>(a.sc, tot);
-  }
-}
-
-int prepare_sym3_chunks(Matrix *m) {
-  const int64_t nn = m->n / 3;
-  std::vector<int32_t> ptr(nn + 1), up(nn + 1);
-  if (cudaMemcpy(ptr.data(), m->nbr_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
-      cudaMemcpy(up.data(), m->up_ptr, (nn + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return B200FEM_E_CUDA;
-  std::vector<int32_t> ch{0};
-  int64_t start = 0;
-  for (int64_t n = 0; n < nn; ++n) {
-    const int64_t nu = up[n + 1] - up[start], nb = ptr[n + 1] - ptr[start];
-    const bool fits = 72 * nu + 32 <= kSymUpBytes && 4 * nb + 32 <= kSymNbrBytes && (n + 1 - start) <= kTmaConsumers;
-    if (!fits) {
-      if (n == start) return 0;
-      ch.push_back((int32_t)n);
-      start = n;
-    }
-  }
-  ch.push_back((int32_t)nn);
-  m->n_chunks = (int)ch.size() - 1;
-  if (dalloc(&m->chunk_node, ch.size()) != cudaSuccess) return B200FEM_E_CUDA;
-  if (cudaMemcpy(m->chunk_node, ch.data(), ch.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess)
-    return B200FEM_E_CUDA;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_JACOBI_R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_JACOBI_TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_RESIDUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(k_spmv_sym3_tma<SP_CGRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    attr = true;
-  }
-  m->use_tma = true;
-  return 0;
-}
-
 
 // ------------------------------------------------------------------------------------
 // GRID3: symmetric storage for z-major box lattices (generate_box_mesh, mesh.py:134-168).
@@ -968,10 +460,18 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
                                                              int node_hi, SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
-  const int lane = threadIdx.x & 31;
+  // The epilogue's row operands (D^-1, r0 / s / b, ...) of the warp's 96 chunk rows are copied
+  // into shared memory with cp.async when the chunk starts, so their latency hides behind the
+  // 27 block products without holding registers: the 255-register budget stays with the block
+  // loads in flight (preloading them into registers cost the Jacobi-mode matvecs +15 %,
+  // 531 / 548 us against 463 us plain at config 3, profiles/r02_krylov_profile.json).
+  constexpr int NE = n_ext<MODE>();
+  __shared__ double s_ext[kGThreads / 32][NE > 0 ? NE : 1][96];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   const int64_t np = g.npad;
+  const int64_t n_rows = 3 * (int64_t)g.nn;
   double red0 = 0.0, red1 = 0.0;
   const int nch = (int)(np >> 5);
   const SlabWalk sw = slab_walk(g, node_lo, node_hi);
@@ -979,57 +479,75 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
     int lo, hi;
     const int c = sw.chunk(w, g, node_lo, node_hi, lo, hi);
     const int c0 = c << 5, node = c0 + lane;
-    if (node < lo || node >= hi) continue;
-    const LatticePos p = lattice_pos(node, c0, g);
-    const double *__restrict__ x = a.x;
-    // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
-    // their latency hides behind the 27 block products instead of trailing them
-    RowPre pre[3];
-    bool dfl[3];
+    const bool active = node >= lo && node < hi;
+    if (NE > 0) {
+      const int64_t r0 = 3 * (int64_t)c0;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      pre[r] = spmv_preload<MODE>(3 * (int64_t)node + r, a);
-      dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
+      for (int e = 0; e < NE; ++e) {
+        const double *src = ext_ptr<MODE>(a, e) + r0;
+#pragma unroll
+        for (int t = lane; t < 96; t += 32)
+          if (r0 + t < n_rows) cp_async8(&s_ext[wib][e][t], src + t);
+      }
+      cp_async_commit();
     }
-    double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
+    double acc[3] = {0.0, 0.0, 0.0};
+    if (active) {
+      const LatticePos p = lattice_pos(node, c0, g);
+      const double *__restrict__ x = a.x;
+      bool dfl[3];
 #pragma unroll
-    for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
-      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
-      const bool ok = grid_has(p, di, dj, dk);
-      const int m = node + di + dj * g.nx + dk * g.nxy;
-      VT b[9];
-      double xm[3];
-      grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
+      for (int r = 0; r < 3; ++r) dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
+      double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+      for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
+        const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+        const bool ok = grid_has(p, di, dj, dk);
+        const int m = node + di + dj * g.nx + dk * g.nxy;
+        VT b[9];
+        double xm[3];
+        grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
-        yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
+        for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
+      }
+      // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
+      // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
+      // read may come first; an evict-first line would then be dropped before that second use
+      // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
+#pragma unroll
+      for (int q = 1; q < 14; ++q) {
+        const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+        const bool ok = grid_has(p, -di, -dj, -dk);
+        const int m = node - di - dj * g.nx - dk * g.nxy;
+        VT b[9];
+        double xm[3];
+        grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) acc[r] = dfl[r] ? __ldg(x + 3 * (int64_t)node + r) : yu[r] + yl[r];
     }
-#pragma unroll
-    // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
-    // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
-    // read may come first; an evict-first line would then be dropped before that second use
-    // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
-    for (int q = 1; q < 14; ++q) {
-      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
-      const bool ok = grid_has(p, -di, -dj, -dk);
-      const int m = node - di - dj * g.nx - dk * g.nxy;
-      VT b[9];
-      double xm[3];
-      grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);  // normal policy (see below)
-#pragma unroll
-      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-        yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
+    if (NE > 0) {
+      cp_async_wait_all();
+      __syncwarp();
     }
+    if (active) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int64_t row = 3 * (int64_t)node + r;
-      const double acc = dfl[r] ? __ldg(x + row) : yu[r] + yl[r];
-      spmv_epilogue<MODE>(row, acc, a, pre[r], red0, red1);
+      for (int r = 0; r < 3; ++r) {
+        const int t = 3 * lane + r;
+        const RowPre pre = row_pre_from<MODE>(&s_ext[wib][0][t], &s_ext[wib][NE > 1 ? 1 : 0][t],
+                                              &s_ext[wib][NE > 2 ? 2 : 0][t]);
+        spmv_epilogue<MODE>(3 * (int64_t)node + r, acc[r], a, pre, red0, red1);
+      }
     }
+    if (NE > 0) __syncwarp();  // the next chunk's copies overwrite s_ext
   }
   if (MODE != SP_PLAIN) {
     double v2[2] = {red0, red1}, tot[2];
@@ -1184,22 +702,12 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
       count_launch();
       return;
     }
-    switch (tma_x_variant()) {
-      case 1: k_spmv_fem3_tma<MODE, 1><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
-                                                                                m->n_chunks, m->nnz / 9, m->n, a, r); break;
-      case 2: k_spmv_fem3_tma<MODE, 2><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
-                                                                                m->n_chunks, m->nnz / 9, m->n, a, r); break;
-      default: k_spmv_fem3_tma<MODE, 0><<<g, kTmaThreads, kTmaSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->data, m->chunk_node,
-                                                                                 m->n_chunks, m->nnz / 9, m->n, a, r);
-    }
+    launch_fem3_tma_npw1(m, MODE, a, r, g);  // spmv_alt.cu
   } else if (m->kind == MK_SYM3 && m->use_tma && full) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int g = std::min(sms, m->n_chunks);
-    k_spmv_sym3_tma<MODE><<<g, kTmaThreads, kSymSmem, m->stream>>>(m->nbr_ptr, m->nbr, m->up_ptr, m->lo_blk, m->data,
-                                                                  m->dir_flag, m->chunk_node, m->n_chunks, m->n / 3,
-                                                                  a, r);
+    launch_sym3_tma(m, MODE, a, r, std::min(sms, m->n_chunks));  // spmv_alt.cu
   } else if (m->kind == MK_SYM3) {
     const int64_t lo = full ? 0 : m->row_lo, hi = full ? m->n / 3 : m->row_hi;
     k_spmv_sym3<MODE><<<grid, kThreads, 0, m->stream>>>(m->nbr_ptr, m->nbr, m->up_ptr, m->lo_blk, m->data,
