@@ -790,7 +790,6 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
   {  // ---- 1. lane (c, q): point quantities and the per-node vectors
     const int q = a8;
     double Jm[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    double Gr[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // sum_k U_k (x) dphi_k (reference gradient)
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const double d0 = sdN[q * 25 + k * 3], d1 = sdN[q * 25 + k * 3 + 1], d2 = sdN[q * 25 + k * 3 + 2];
@@ -800,13 +799,6 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
         Jm[i][0] = fma(x, d0, Jm[i][0]);
         Jm[i][1] = fma(x, d1, Jm[i][1]);
         Jm[i][2] = fma(x, d2, Jm[i][2]);
-      }
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const double u = sXUw[c][k][3 + v];
-        Gr[v][0] = fma(u, d0, Gr[v][0]);
-        Gr[v][1] = fma(u, d1, Gr[v][1]);
-        Gr[v][2] = fma(u, d2, Gr[v][2]);
       }
     }
     const double A0 = Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1], B0 = Jm[0][2] * Jm[2][1] - Jm[0][1] * Jm[2][2];
@@ -820,15 +812,26 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
     const double inv[3][3] = {{A0 * r, B0 * r, C0 * r}, {D0 * r, E0 * r, F0 * r}, {G0 * r, H0 * r, I0 * r}};
     double scale = jxw;
     if (a.mp.simp) scale *= pow(a.theta[e], a.mp.penalty);
-    double gu[3][3];
+    // physical gradients and grad u = sum_k U_k (x) G_k in the residual kernel's operation order
+    // (qp_geometry, k_residual): R and K see the same grad u to the last bit, which matters at
+    // knife edges such as the J2 yield test f == 0 (reference tests/test_materials.py:199-210)
+    double G[8][3];
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double d0 = sdN[q * 25 + k * 3], d1 = sdN[q * 25 + k * 3 + 1], d2 = sdN[q * 25 + k * 3 + 2];
+#pragma unroll
+      for (int aa = 0; aa < 3; ++aa) G[k][aa] = inv[0][aa] * d0 + inv[1][aa] * d1 + inv[2][aa] * d2;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gu[v][d] = fma(sXUw[c][k][3 + v], G[k][d], gu[v][d]);
+    }
     double gs = 0.0;
 #pragma unroll
     for (int v = 0; v < VEC; ++v)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        gu[v][d] = Gr[v][0] * inv[0][d] + Gr[v][1] * inv[1][d] + Gr[v][2] * inv[2][d];
-        gs += fabs(gu[v][d]);
-      }
+      for (int d = 0; d < 3; ++d) gs += fabs(gu[v][d]);
     bool vfin = isfinite(gs), fin = true, bad_def = false;
     double detF = 1.0;
     double cf[4] = {0.0, 0.0, 0.0, 0.0};
@@ -900,10 +903,7 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
     double *Vq = V + c * CS + q * QS;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const double d0 = sdN[q * 25 + k * 3], d1 = sdN[q * 25 + k * 3 + 1], d2 = sdN[q * 25 + k * 3 + 2];
-      double g[3];
-#pragma unroll
-      for (int aa = 0; aa < 3; ++aa) g[aa] = inv[0][aa] * d0 + inv[1][aa] * d1 + inv[2][aa] * d2;
+      const double g[3] = {G[k][0], G[k][1], G[k][2]};
 #pragma unroll
       for (int d = 0; d < 3; ++d) Vq[k * NV + d] = g[d];
       if (MAT == B200FEM_MAT_NH) {  // h = H g (slot 3), u = F g (slot 6)
