@@ -460,18 +460,10 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
                                                              int node_hi, SpmvArgs a, RedScratch red) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
-  // The epilogue's row operands (D^-1, r0 / s / b, ...) of the warp's 96 chunk rows are copied
-  // into shared memory with cp.async when the chunk starts, so their latency hides behind the
-  // 27 block products without holding registers: the 255-register budget stays with the block
-  // loads in flight (preloading them into registers cost the Jacobi-mode matvecs +15 %,
-  // 531 / 548 us against 463 us plain at config 3, profiles/r02_krylov_profile.json).
-  constexpr int NE = n_ext<MODE>();
-  __shared__ double s_ext[kGThreads / 32][NE > 0 ? NE : 1][96];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   const int64_t np = g.npad;
-  const int64_t n_rows = 3 * (int64_t)g.nn;
   double red0 = 0.0, red1 = 0.0;
   const int nch = (int)(np >> 5);
   const SlabWalk sw = slab_walk(g, node_lo, node_hi);
@@ -479,75 +471,57 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
     int lo, hi;
     const int c = sw.chunk(w, g, node_lo, node_hi, lo, hi);
     const int c0 = c << 5, node = c0 + lane;
-    const bool active = node >= lo && node < hi;
-    if (NE > 0) {
-      const int64_t r0 = 3 * (int64_t)c0;
+    if (node < lo || node >= hi) continue;
+    const LatticePos p = lattice_pos(node, c0, g);
+    const double *__restrict__ x = a.x;
+    // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
+    // their latency hides behind the 27 block products instead of trailing them
+    RowPre pre[3];
+    bool dfl[3];
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const double *src = ext_ptr<MODE>(a, e) + r0;
-#pragma unroll
-        for (int t = lane; t < 96; t += 32)
-          if (r0 + t < n_rows) cp_async8(&s_ext[wib][e][t], src + t);
-      }
-      cp_async_commit();
+    for (int r = 0; r < 3; ++r) {
+      pre[r] = spmv_preload<MODE>(3 * (int64_t)node + r, a);
+      dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
     }
-    double acc[3] = {0.0, 0.0, 0.0};
-    if (active) {
-      const LatticePos p = lattice_pos(node, c0, g);
-      const double *__restrict__ x = a.x;
-      bool dfl[3];
+    double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int r = 0; r < 3; ++r) dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
-      double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
+    for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, di, dj, dk);
+      const int m = node + di + dj * g.nx + dk * g.nxy;
+      VT b[9];
+      double xm[3];
+      grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
 #pragma unroll
-      for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
-        const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
-        const bool ok = grid_has(p, di, dj, dk);
-        const int m = node + di + dj * g.nx + dk * g.nxy;
-        VT b[9];
-        double xm[3];
-        grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-          yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
-      }
-      // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
-      // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
-      // read may come first; an evict-first line would then be dropped before that second use
-      // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
-#pragma unroll
-      for (int q = 1; q < 14; ++q) {
-        const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
-        const bool ok = grid_has(p, -di, -dj, -dk);
-        const int m = node - di - dj * g.nx - dk * g.nxy;
-        VT b[9];
-        double xm[3];
-        grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-          yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
-      }
-#pragma unroll
-      for (int r = 0; r < 3; ++r) acc[r] = dfl[r] ? __ldg(x + 3 * (int64_t)node + r) : yu[r] + yl[r];
+      for (int r = 0; r < 3; ++r)
+        yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
     }
-    if (NE > 0) {
-      cp_async_wait_all();
-      __syncwarp();
-    }
-    if (active) {
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int t = 3 * lane + r;
-        const RowPre pre = row_pre_from<MODE>(&s_ext[wib][0][t], &s_ext[wib][NE > 1 ? 1 : 0][t],
-                                              &s_ext[wib][NE > 2 ? 2 : 0][t]);
-        spmv_epilogue<MODE>(3 * (int64_t)node + r, acc[r], a, pre, red0, red1);
-      }
+    // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
+    // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
+    // read may come first; an evict-first line would then be dropped before that second use
+    // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
+    for (int q = 1; q < 14; ++q) {
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, -di, -dj, -dk);
+      const int m = node - di - dj * g.nx - dk * g.nxy;
+      VT b[9];
+      double xm[3];
+      grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);  // normal policy (see below)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
     }
-    if (NE > 0) __syncwarp();  // the next chunk's copies overwrite s_ext
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t row = 3 * (int64_t)node + r;
+      const double acc = dfl[r] ? __ldg(x + row) : yu[r] + yl[r];
+      spmv_epilogue<MODE>(row, acc, a, pre[r], red0, red1);
+    }
   }
   if (MODE != SP_PLAIN) {
     double v2[2] = {red0, red1}, tot[2];
