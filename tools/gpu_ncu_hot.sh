@@ -1,0 +1,16 @@
+#!/bin/bash
+# ncu --set full of the config-3 hot kernels (one launch each), after a clean run of the same script.
+cd "$(dirname "$0")/.."
+O=gpurun_out
+export B200FEM_NO_GRAPH=1
+python tools/ncu_targets.py all > $O/c5_targets.log 2>&1 || exit 1
+ncu --set full --clock-control none --import-source on -k regex:'k_jacobian_v2|k_grid_pull' -c 2 \
+    -o $O/r02_ncu_tangent python tools/ncu_targets.py tangent > $O/c5_ncu_tangent.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'k_residual' -c 2 \
+    -o $O/r02_ncu_residual python tools/ncu_targets.py residual > $O/c5_ncu_residual.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'k_spmv_grid3' -c 4 \
+    -o $O/r02_ncu_spmv python tools/ncu_targets.py spmv > $O/c5_ncu_spmv.log 2>&1
+for f in tangent residual spmv; do
+  ncu -i $O/r02_ncu_$f.ncu-rep --page raw --csv > $O/r02_ncu_${f}_raw.csv 2>/dev/null
+done
+ls -la $O
