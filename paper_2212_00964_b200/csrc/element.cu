@@ -1007,7 +1007,31 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, 
     double K[NB][BB];
     jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
     const int ia = lane & 7;
-    if (valid) {
+    if (soa) {
+      // element-major scratch [pair][VV][cell] for the lattice pull: stage the warp's 4 cells
+      // in shared memory (the V region is free once the pair loop is done), then write every
+      // (pair, entry) as the 4 consecutive cells -- full 32-byte sectors instead of the partial
+      // sectors of per-lane 8-byte stores, and coalesced reads for the pull's thread per node
+      __syncwarp();
+      double *stg = V;  // 36 * BB * 4 doubles <= 4 * CS
+#pragma unroll
+      for (int d = 0; d < NB; ++d) {
+        if (d == 4 && ia >= 4) break;
+        const int b = (ia + d) & 7;
+        const int lo = ia < b ? ia : b, hi = ia < b ? b : ia;
+        const int p = lo * (15 - lo) / 2 + hi;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+#pragma unroll
+          for (int k = 0; k < VEC; ++k)
+            stg[((p * BB) + i * VEC + k) * 4 + c] = (ia <= b) ? K[d][i * VEC + k] : K[d][k * VEC + i];
+      }
+      __syncwarp();
+      for (int t = lane; t < 36 * BB * 4; t += 32) {
+        const int pe = t >> 2, cc = t & 3;
+        if (base + cc < n) Ke[(int64_t)pe * n + base + cc] = stg[t];
+      }
+    } else if (valid) {
 #pragma unroll
       for (int d = 0; d < NB; ++d) {
         if (d == 4 && ia >= 4) break;
@@ -1772,7 +1796,9 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
   // Not for vec 3: a thread's 27 blocks land in 3 rows ~2 KB apart from its neighbours' -- the
   // uncoalesced 8-byte stores made it 21 ms against 13.7 ms for the gather (config 3)
   const bool csr_pull = !grid && data && !sym && c->grid_nx && c->vec == 1 && !getenv("B200FEM_NO_GRID_PULL");
-  const int soa = ((pull || csr_pull) && c->vec == 1) ? 1 : 0;
+  // element-major scratch for the lattice pulls: vec 1 always; vec 3 when the node-lane phase A
+  // writes it (staged, full-sector stores; the pair-per-lane v1 kernel keeps cell-major blocks)
+  const int soa = ((pull || csr_pull) && (c->vec == 1 || tangent_variant() != 0)) ? 1 : 0;
   if (tangent_variant() == 0) {  // A/B: the pair-per-lane phase A
     const int g = grid_cap(c->n_cells, kJacWarps);
     switch (c->material) {
@@ -1793,7 +1819,10 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
   if (pull) {
     const int64_t nn = c->n_nodes;
     const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nn + kThreads - 1) / kThreads));
-    if (c->vec == 3)
+    if (c->vec == 3 && soa)
+      k_grid_pull<3, true><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
+                                                   c->grid_npad, grid);
+    else if (c->vec == 3)
       k_grid_pull<3, false><<<gp, kThreads, 0, s>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny, c->grid_nz,
                                                     c->grid_npad, grid);
     else

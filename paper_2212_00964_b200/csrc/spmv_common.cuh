@@ -14,22 +14,24 @@ struct RowPre {
 
 template <int MODE>
 __device__ __forceinline__ RowPre spmv_preload(int64_t i, const SpmvArgs &a) {
+  // row operands are read once per matvec: evict-first (__ldcs) so they do not push the
+  // matrix blocks a GRID3 matvec re-reads from L2 (its lower blocks) out of the cache
   RowPre p{0.0, 0.0, 0.0, 0.0};
   if (MODE == SP_JACOBI_R0) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
+    p.inv = __ldcs(a.inv + i);
+    p.aux = __ldcs(a.aux + i);
   } else if (MODE == SP_JACOBI_TT) {
-    p.inv = __ldg(a.inv + i);
+    p.inv = __ldcs(a.inv + i);
     p.xi = __ldg(a.x + i);
   } else if (MODE == SP_RESIDUAL) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
-    p.dg = __ldg(a.dg + i);
+    p.inv = __ldcs(a.inv + i);
+    p.aux = __ldcs(a.aux + i);
+    p.dg = __ldcs(a.dg + i);
   } else if (MODE == SP_PQ) {
     p.xi = __ldg(a.x + i);
   } else if (MODE == SP_CGRES) {
-    p.inv = __ldg(a.inv + i);
-    p.aux = __ldg(a.aux + i);
+    p.inv = __ldcs(a.inv + i);
+    p.aux = __ldcs(a.aux + i);
   }
   return p;
 }
