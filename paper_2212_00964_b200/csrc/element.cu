@@ -762,7 +762,10 @@ struct Jac2Cfg {
   static constexpr int CS = 8 * QS;       // cell stride = 64 NV + 8 = 8 (mod 16): two cells 16 banks apart
   static_assert(CS % 16 == 8, "cell stride must be 8 mod 16 doubles");
   // dynamic shared memory (doubles): dN table [q][25] | X,U [w][c][k][7] | V [w][4 CS] | coef [w][160]
-  static constexpr int SM_DN = 8 * 25, SM_XU = kJac2Warps * 4 * 8 * 7, SM_V = kJac2Warps * 4 * CS,
+  // per-warp V region, also the staging buffer of the element-major scratch stores (36 pairs x
+  // VEC^2 entries x 4 cells): the larger of the two
+  static constexpr int VW = (4 * CS > 36 * VEC * VEC * 4) ? 4 * CS : 36 * VEC * VEC * 4;
+  static constexpr int SM_DN = 8 * 25, SM_XU = kJac2Warps * 4 * 8 * 7, SM_V = kJac2Warps * VW,
                        SM_C = kJac2Warps * 160;
   static constexpr size_t BYTES = sizeof(double) * (SM_DN + SM_XU + SM_V + SM_C);
 };
@@ -997,7 +1000,7 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, 
   for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3;
-  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * 4 * CS;                  // [c][q][a][NV]
+  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * CF::VW;                  // [c][q][a][NV]
   double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;         // [c][q][4], point stride 5
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1615,7 +1618,7 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 1) k_tangent_grid_fused(ElemA
   for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_NEXT; t += blockDim.x) nxt[t] = 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3, ia = lane & 7;
-  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * 4 * CS;
+  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * CF::VW;
   double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;
   const int nxc = NX - 1, nyc = NY - 1, nzc = NZ - 1;
   const int mx = (nxc + kFT - 1) / kFT;
