@@ -455,7 +455,7 @@ __device__ __forceinline__ void grid_block(const float *__restrict__ grid, int64
 
 // VT = double: the stored tangent.  VT = float: its single-precision copy (opt-in
 // operator "grid32", b200fem_matrix_set_f32): half the value bytes, products and sums in FP64.
-template <int MODE, typename VT, bool LATE = false>
+template <int MODE, typename VT>
 __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : kGMinBlocks) k_spmv_grid3(const VT *__restrict__ grid, GridDims g,
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
                                                              int node_hi, SpmvArgs a, RedScratch red) {
@@ -476,12 +476,11 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
     const double *__restrict__ x = a.x;
     // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
     // their latency hides behind the 27 block products instead of trailing them
-    // (LATE: A/B variant that loads them after the block products, B200FEM_GRID_LATE_EPI=1)
     RowPre pre[3];
     bool dfl[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      if (!LATE) pre[r] = spmv_preload<MODE>(3 * (int64_t)node + r, a);
+      pre[r] = spmv_preload<MODE>(3 * (int64_t)node + r, a);
       dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
     }
     double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
@@ -521,7 +520,6 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
     for (int r = 0; r < 3; ++r) {
       const int64_t row = 3 * (int64_t)node + r;
       const double acc = dfl[r] ? __ldg(x + row) : yu[r] + yl[r];
-      if (LATE) pre[r] = spmv_preload<MODE>(row, a);
       spmv_epilogue<MODE>(row, acc, a, pre[r], red0, red1);
     }
   }
@@ -644,12 +642,6 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   }
 }
 
-static bool grid_late_epilogue() {
-  static int v = -1;
-  if (v < 0) v = getenv("B200FEM_GRID_LATE_EPI") ? 1 : 0;
-  return v == 1;
-}
-
 template <int MODE>
 static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
@@ -670,8 +662,6 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
       if (m->data32)
         k_spmv_grid3<MODE, float><<<(int)std::min<int64_t>((int64_t)kGMinBlocks32 * gg, std::max(1, (nch + 7) / 8)),
                                     kGThreads, 0, m->stream>>>(m->data32, g, m->dir_flag, lo, hi, a, r);
-      else if (MODE != SP_PLAIN && grid_late_epilogue())
-        k_spmv_grid3<MODE, double, true><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
       else
         k_spmv_grid3<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
     }
