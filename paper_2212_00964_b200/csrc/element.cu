@@ -752,22 +752,21 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
 //   J2:  K_ik += c1 d_ik (g_a.g_b) + cl g_a,i g_b,k + c1 g_a,k g_b,i + c3 y_a,i y_b,k
 //   LE:  J2 without the y term;  Poisson: c1 (g_a.g_b)
 // Shared-memory strides are padded so that every access pattern is bank-conflict free.
-constexpr int kJac2Warps = 2;  // 64-thread CTAs: 5 per SM fit 228 KB of shared memory and 204 registers
-constexpr int kFWarps = 4;     // the fused column kernel: 16 cells per colour round
-constexpr int kXP = 6;         // X,U row pitch (doubles)
+constexpr int kJac2Warps = 4;
 
-template <int MAT, int W = kJac2Warps>
+template <int MAT>
 struct Jac2Cfg {
   static constexpr int VEC = (MAT == B200FEM_MAT_POISSON) ? 1 : 3;
   static constexpr int NV = (MAT == B200FEM_MAT_NH) ? 9 : (MAT == B200FEM_MAT_J2) ? 6 : 3;  // vector doubles
   static constexpr int QS = 8 * NV + 1;   // point stride (odd: conflict-free across points)
   static constexpr int CS = 8 * QS;       // cell stride = 64 NV + 8 = 8 (mod 16): two cells 16 banks apart
   static_assert(CS % 16 == 8, "cell stride must be 8 mod 16 doubles");
-  // dynamic shared memory (doubles): dN table [q][25] | X,U [w][c][k][kXP] | V [w][VW] | coef [w][128]
+  // dynamic shared memory (doubles): dN table [q][25] | X,U [w][c][k][7] | V [w][4 CS] | coef [w][160]
   // per-warp V region, also the staging buffer of the element-major scratch stores (36 pairs x
   // VEC^2 entries x 4 cells): the larger of the two
   static constexpr int VW = (4 * CS > 36 * VEC * VEC * 4) ? 4 * CS : 36 * VEC * VEC * 4;
-  static constexpr int SM_DN = 8 * 25, SM_XU = W * 4 * 8 * kXP, SM_V = W * VW, SM_C = W * 128;
+  static constexpr int SM_DN = 8 * 25, SM_XU = kJac2Warps * 4 * 8 * 7, SM_V = kJac2Warps * VW,
+                       SM_C = kJac2Warps * 160;
   static constexpr size_t BYTES = sizeof(double) * (SM_DN + SM_XU + SM_V + SM_C);
 };
 
@@ -777,7 +776,7 @@ struct Jac2Cfg {
 // flagged on the device (DevErr) exactly as the other element kernels do.
 template <int MAT>
 __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, bool valid, int lane,
-                                                 const double *__restrict__ sdN, double (*sXUw)[8][kXP], double *V,
+                                                 const double *__restrict__ sdN, double (*sXUw)[8][7], double *V,
                                                  double *Cf, double (&K)[5][Jac2Cfg<MAT>::VEC * Jac2Cfg<MAT>::VEC]) {
   using CF = Jac2Cfg<MAT>;
   constexpr int VEC = CF::VEC, NV = CF::NV, QS = CF::QS, CS = CF::CS;
@@ -903,7 +902,7 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) Cf[c * 32 + q * 4 + j] = cf[j];
+    for (int j = 0; j < 4; ++j) Cf[c * 40 + q * 5 + j] = cf[j];
     double *Vq = V + c * CS + q * QS;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -932,8 +931,8 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
 #pragma unroll 1
   for (int q = 0; q < 8; ++q) {
     const double *Vq = V + c * CS + q * QS;
-    const double c1 = Cf[c * 32 + q * 4], c2 = Cf[c * 32 + q * 4 + 1], c3 = Cf[c * 32 + q * 4 + 2],
-                 c4 = Cf[c * 32 + q * 4 + 3];
+    const double c1 = Cf[c * 40 + q * 5], c2 = Cf[c * 40 + q * 5 + 1], c3 = Cf[c * 40 + q * 5 + 2],
+                 c4 = Cf[c * 40 + q * 5 + 3];
     double va[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) va[j] = Vq[ia * NV + j];
@@ -990,19 +989,19 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
 }
 
 template <int MAT>
-__global__ void __launch_bounds__(kJac2Warps * 32, 5) k_jacobian_v2(ElemArgs a, int64_t n, double *__restrict__ Ke,
+__global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, int64_t n, double *__restrict__ Ke,
                                                                     int soa) {
   using CF = Jac2Cfg<MAT>;
   constexpr int VEC = CF::VEC, CS = CF::CS;
   constexpr int NB = 5, BB = VEC * VEC;
   extern __shared__ double jac2_sm[];
   double *sdN = jac2_sm;                                                     // [q][k*3 + d], point stride 25
-  double(*sXU)[4][8][kXP] = reinterpret_cast<double(*)[4][8][kXP]>(jac2_sm + CF::SM_DN);  // [w][c][k][X, U]
+  double(*sXU)[4][8][7] = reinterpret_cast<double(*)[4][8][7]>(jac2_sm + CF::SM_DN);  // [w][c][k][X, U]
   for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3;
   double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * CF::VW;                  // [c][q][a][NV]
-  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 128;         // [c][q][4]
+  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;         // [c][q][4], point stride 5
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
@@ -1587,7 +1586,7 @@ constexpr int kFNext = 5 * 9;                  // in-plane blocks carried to the
 
 template <int MAT>
 struct FusedCfg {
-  using CF = Jac2Cfg<MAT, kFWarps>;
+  using CF = Jac2Cfg<MAT>;
   static constexpr int SM_ACC = kFNodes * kFAcc, SM_NEXT = kFNodes * kFNext;
   static constexpr size_t BYTES = CF::BYTES + sizeof(double) * (SM_ACC + SM_NEXT);
 };
@@ -1603,15 +1602,15 @@ __device__ __forceinline__ int64_t edge_line(int i, int j, int NX, int NY) {
 }
 
 template <int MAT>
-__global__ void __launch_bounds__(kFWarps * 32, 1) k_tangent_grid_fused(ElemArgs a, int NX, int NY, int NZ,
+__global__ void __launch_bounds__(kJac2Warps * 32, 1) k_tangent_grid_fused(ElemArgs a, int NX, int NY, int NZ,
                                                                            int64_t gnpad, double *__restrict__ grid,
                                                                            double *__restrict__ part) {
-  using CF = Jac2Cfg<MAT, kFWarps>;
+  using CF = Jac2Cfg<MAT>;
   static_assert(CF::VEC == 3, "vec-3 laws only");
   constexpr int CS = CF::CS;
   extern __shared__ double jac2_sm[];
   double *sdN = jac2_sm;
-  double(*sXU)[4][8][kXP] = reinterpret_cast<double(*)[4][8][kXP]>(jac2_sm + CF::SM_DN);
+  double(*sXU)[4][8][7] = reinterpret_cast<double(*)[4][8][7]>(jac2_sm + CF::SM_DN);
   double *acc = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + CF::SM_C;  // [node][14 kinds][9], stride kFAcc
   double *nxt = acc + FusedCfg<MAT>::SM_ACC;                             // [node][5 kinds][9]
   for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
@@ -1620,7 +1619,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 1) k_tangent_grid_fused(ElemArgs
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3, ia = lane & 7;
   double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * CF::VW;
-  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 128;
+  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;
   const int nxc = NX - 1, nyc = NY - 1, nzc = NZ - 1;
   const int mx = (nxc + kFT - 1) / kFT;
   const int tx = blockIdx.x % mx, ty = blockIdx.x / mx;
@@ -1638,7 +1637,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 1) k_tangent_grid_fused(ElemArgs
       const int64_t n = i + (int64_t)NX * j + nxy * pk;
       grid[grid_idx(kind, ke % 9, n, gnpad)] = acc[node * kFAcc + ke];
     }
-    for (int node = w; node < kFNodes; node += kFWarps) {  // warp per side-face node
+    for (int node = w; node < kFNodes; node += kJac2Warps) {  // warp per side-face node
       const int li = node % kFN, lj = node / kFN, i = i0 + li, j = j0 + lj;
       if (i >= NX || j >= NY) continue;
       const int64_t line = edge_line(i, j, NX, NY);
@@ -1739,7 +1738,7 @@ static void launch_fused(Ctx *c, cudaStream_t s, const ElemArgs &a, double *grid
     attr = true;
   }
   const int mx = (c->grid_nx - 1 + kFT - 1) / kFT, my = (c->grid_ny - 1 + kFT - 1) / kFT;
-  k_tangent_grid_fused<MAT><<<mx * my, kFWarps * 32, FusedCfg<MAT>::BYTES, s>>>(
+  k_tangent_grid_fused<MAT><<<mx * my, kJac2Warps * 32, FusedCfg<MAT>::BYTES, s>>>(
       a, c->grid_nx, c->grid_ny, c->grid_nz, c->grid_npad, grid, c->scratch);
   const int64_t total = fused_part_doubles(c->grid_nx, c->grid_ny, c->grid_nz) / 4;
   if (total > 0)
