@@ -251,12 +251,6 @@ static void free_ctx(Ctx *c) {
   if (c->indices && c->indices != c->nbr) cudaFree(c->indices);
   red_free(&c->red);
   if (c->pinned) cudaFreeHost(c->pinned);
-  if (c->aux_stream) {
-    cudaStreamSynchronize(c->aux_stream);
-    cudaStreamDestroy(c->aux_stream);
-    for (cudaEvent_t e : c->aux_ev)
-      if (e) cudaEventDestroy(e);
-  }
   delete c;
 }
 

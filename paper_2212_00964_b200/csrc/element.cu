@@ -990,7 +990,7 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
 
 template <int MAT>
 __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, int64_t n, double *__restrict__ Ke,
-                                                                    int soa, int64_t cell_lo, int64_t cell_hi) {
+                                                                    int soa) {
   using CF = Jac2Cfg<MAT>;
   constexpr int VEC = CF::VEC, CS = CF::CS;
   constexpr int NB = 5, BB = VEC * VEC;
@@ -1004,10 +1004,9 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, 
   double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;         // [c][q][4], point stride 5
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // cells [cell_lo, cell_hi) of n (cell_lo a multiple of 4: full-sector element-major stores)
-  for (int64_t base = cell_lo + warp0 * 4; base < cell_hi; base += nwarps * 4) {
-    const bool valid = base + c < cell_hi;
-    const int64_t e = valid ? base + c : cell_hi - 1;
+  for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
+    const bool valid = base + c < n;
+    const int64_t e = valid ? base + c : n - 1;
     double K[NB][BB];
     jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
     const int ia = lane & 7;
@@ -1033,7 +1032,7 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, 
       __syncwarp();
       for (int t = lane; t < 36 * BB * 4; t += 32) {
         const int pe = t >> 2, cc = t & 3;
-        if (base + cc < cell_hi) Ke[(int64_t)pe * n + base + cc] = stg[t];
+        if (base + cc < n) Ke[(int64_t)pe * n + base + cc] = stg[t];
       }
     } else if (valid) {
 #pragma unroll
@@ -1452,12 +1451,11 @@ __device__ __forceinline__ int vtk_local(int lx, int ly, int lz) {  // HEX8 vert
 
 template <int VEC, bool SOA>
 __global__ void __launch_bounds__(kThreads) k_grid_pull(const double *__restrict__ Ke, int64_t n_cells, int NX,
-                                                        int NY, int NZ, int64_t gnpad, double *__restrict__ grid,
-                                                        int64_t node_lo = 0, int64_t node_hi = -1) {
+                                                        int NY, int NZ, int64_t gnpad, double *__restrict__ grid) {
   constexpr int VV = VEC * VEC;
-  const int64_t nn = node_hi < 0 ? (int64_t)NX * NY * NZ : node_hi;
+  const int64_t nn = (int64_t)NX * NY * NZ;
   const int cx_n = NX - 1, cy_n = NY - 1, cz_n = NZ - 1;
-  for (int64_t n = node_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nn; n += (int64_t)gridDim.x * blockDim.x) {
     const int kz = (int)(n / ((int64_t)NX * NY)), rem = (int)(n - (int64_t)kz * NX * NY), jy = rem / NX,
               ix = rem - jy * NX;
 #pragma unroll 1
@@ -1750,14 +1748,13 @@ static void launch_fused(Ctx *c, cudaStream_t s, const ElemArgs &a, double *grid
 }
 
 template <int MAT>
-static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, double *Ke, int soa, int64_t lo = 0,
-                        int64_t hi = -1) {
+static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, double *Ke, int soa) {
   static bool attr = false;  // > 48 KB of shared memory is opt-in per kernel
   if (!attr) {
     cudaFuncSetAttribute(k_jacobian_v2<MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Jac2Cfg<MAT>::BYTES);
     attr = true;
   }
-  k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa, lo, hi < 0 ? n : hi);
+  k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
 }
 
 // B200FEM_TANGENT = v2 (default: node-lane phase A) | v1 (pair-per-lane phase A) | fused
@@ -1769,16 +1766,6 @@ static int tangent_variant() {
   if (v < 0) {
     const char *e = getenv("B200FEM_TANGENT");
     v = !e ? 1 : !strcmp(e, "v1") ? 0 : !strcmp(e, "fused") ? 2 : 1;
-  }
-  return v;
-}
-
-// z-slab pipeline depth of the lattice tangent (B200FEM_TANGENT_PIPE=S, 1 = off; at most 16)
-static int tangent_pipeline() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("B200FEM_TANGENT_PIPE");
-    v = e ? std::max(1, std::min(16, atoi(e))) : 1;
   }
   return v;
 }
@@ -1831,47 +1818,6 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
       case B200FEM_MAT_NH: launch_jac2<B200FEM_MAT_NH>(g, s, a, c->n_cells, c->scratch, soa); break;
       default: launch_jac2<B200FEM_MAT_J2>(g, s, a, c->n_cells, c->scratch, soa); break;
     }
-  }
-  if (pull && c->vec == 3 && soa && tangent_pipeline() > 1 && c->grid_nz > 8) {
-    // z-slab pipeline: phase A of cell slab i+1 (main stream) runs while the lattice pull of node
-    // slab i (second stream) streams its scratch -- the pull's DRAM traffic hides behind the
-    // FP64-latency-bound phase A.  Node planes [z_i, z_{i+1}) need cell layers z_i - 1 .. z_{i+1} - 1.
-    const int S = tangent_pipeline();
-    const int nzc = c->grid_nz - 1;
-    const int64_t cpl = (int64_t)(c->grid_nx - 1) * (c->grid_ny - 1), npl = (int64_t)c->grid_nx * c->grid_ny;
-    if (!c->aux_stream) {
-      B200_CUDA_E(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking), err);
-      for (int i = 0; i < 17; ++i) B200_CUDA_E(cudaEventCreateWithFlags(&c->aux_ev[i], cudaEventDisableTiming), err);
-    }
-    B200_CUDA_E(cudaEventRecord(c->aux_ev[16], s), err);  // the pull stream starts after prior work
-    B200_CUDA_E(cudaStreamWaitEvent(c->aux_stream, c->aux_ev[16], 0), err);
-    int64_t cell0 = 0;
-    for (int i = 0; i < S; ++i) {
-      const int z1 = (int)((int64_t)nzc * (i + 1) / S);
-      int64_t cell1 = (i == S - 1) ? c->n_cells : ((cpl * z1 + 3) & ~(int64_t)3);  // multiple of 4
-      if (cell1 > c->n_cells) cell1 = c->n_cells;
-      const int g = grid_cap(std::max<int64_t>(cell1 - cell0, 1), kJac2Warps * 4);
-      switch (c->material) {
-        case B200FEM_MAT_LE: launch_jac2<B200FEM_MAT_LE>(g, s, a, c->n_cells, c->scratch, 1, cell0, cell1); break;
-        case B200FEM_MAT_NH: launch_jac2<B200FEM_MAT_NH>(g, s, a, c->n_cells, c->scratch, 1, cell0, cell1); break;
-        default: launch_jac2<B200FEM_MAT_J2>(g, s, a, c->n_cells, c->scratch, 1, cell0, cell1); break;
-      }
-      B200_CUDA_E(cudaEventRecord(c->aux_ev[i], s), err);
-      B200_CUDA_E(cudaStreamWaitEvent(c->aux_stream, c->aux_ev[i], 0), err);
-      // node planes whose cells are all done: up to z1 (cell layers < z1 complete), all at the end
-      const int p0 = (int)((int64_t)nzc * i / S);
-      const int p1 = (i == S - 1) ? c->grid_nz : z1;
-      const int64_t n0 = npl * (i == 0 ? 0 : p0), n1 = npl * p1;
-      const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (n1 - n0 + 127) / 128));
-      k_grid_pull<3, true><<<gp, 128, 0, c->aux_stream>>>(c->scratch, c->n_cells, c->grid_nx, c->grid_ny,
-                                                          c->grid_nz, c->grid_npad, grid, n0, n1);
-      count_launch(2);
-      cell0 = cell1;
-    }
-    B200_CUDA_E(cudaEventRecord(c->aux_ev[16], c->aux_stream), err);
-    B200_CUDA_E(cudaStreamWaitEvent(s, c->aux_ev[16], 0), err);
-    B200_CUDA_E(cudaGetLastError(), err);
-    return fetch_element_errors(c, err, true);
   }
   if (pull) {
     const int64_t nn = c->n_nodes;

@@ -81,8 +81,6 @@ struct MatParams {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux_stream = nullptr;  // second stream of the pipelined lattice tangent (lazy)
-  cudaEvent_t aux_ev[17]{};
   int64_t n_nodes = 0, n_cells = 0, n_dofs = 0, nnz = 0;
   int vec = 1, material = 0, flags = 0;
   MatParams mp{};
