@@ -1567,186 +1567,6 @@ __global__ void __launch_bounds__(kThreads) k_csr_pull(const double *__restrict_
   }
 }
 
-// ------------------------------------------ fused lattice tangent (GRID3, vec 3, box meshes)
-// One CTA per 8 x 8 column of cells, marching the cell layers k = 0 .. NZ-2.  Per layer the
-// 64 cells are processed in 4 parity colours ((i, j) mod 2: cells of one colour share no node),
-// 16 cells per colour = 4 warps x 4 cells of the phase-A device function above; each lane adds
-// its cell blocks straight into the column's node-block accumulators in shared memory (fixed
-// colour order -> deterministic, no atomics).  Node plane k is complete after layer k (its
-// in-plane blocks carry layer k-1's contributions, its +z blocks have only layer k's), so it is
-// written out as GRID3 blocks and the next plane's in-plane partial sums become the carry.
-// The 6.5 GB per-cell block scratch and the lattice pull of the two-phase path disappear; only
-// nodes on the column's side faces (shared with a neighbouring column) are written as per-column
-// partial blocks and summed by k_grid_edge_finish in a fixed column order.
-constexpr int kFT = 8;                         // cells per column side
-constexpr int kFN = kFT + 1;                   // nodes per column side
-constexpr int kFNodes = kFN * kFN;             // 81
-constexpr int kFAcc = 14 * 9 + 1;              // node stride of the plane accumulator (odd)
-constexpr int kFNext = 5 * 9;                  // in-plane blocks carried to the next plane
-
-template <int MAT>
-struct FusedCfg {
-  using CF = Jac2Cfg<MAT>;
-  static constexpr int SM_ACC = kFNodes * kFAcc, SM_NEXT = kFNodes * kFNext;
-  static constexpr size_t BYTES = CF::BYTES + sizeof(double) * (SM_ACC + SM_NEXT);
-};
-
-// which side-face "edge line" a lattice node (i, j) lies on, or -1 (interior / mesh boundary);
-// x-lines (i = kFT m, 0 < i < nxc) first, then y-lines (j = kFT l, 0 < j < nyc)
-__device__ __forceinline__ int64_t edge_line(int i, int j, int NX, int NY) {
-  const int nxc = NX - 1, nyc = NY - 1;
-  const int mx = (nxc + kFT - 1) / kFT;
-  if (i % kFT == 0 && i > 0 && i < nxc) return (int64_t)(i / kFT - 1) * NY + j;
-  if (j % kFT == 0 && j > 0 && j < nyc) return (int64_t)(mx - 1) * NY + (int64_t)(j / kFT - 1) * NX + i;
-  return -1;
-}
-
-template <int MAT>
-__global__ void __launch_bounds__(kJac2Warps * 32, 1) k_tangent_grid_fused(ElemArgs a, int NX, int NY, int NZ,
-                                                                           int64_t gnpad, double *__restrict__ grid,
-                                                                           double *__restrict__ part) {
-  using CF = Jac2Cfg<MAT>;
-  static_assert(CF::VEC == 3, "vec-3 laws only");
-  constexpr int CS = CF::CS;
-  extern __shared__ double jac2_sm[];
-  double *sdN = jac2_sm;
-  double(*sXU)[4][8][7] = reinterpret_cast<double(*)[4][8][7]>(jac2_sm + CF::SM_DN);
-  double *acc = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + CF::SM_C;  // [node][14 kinds][9], stride kFAcc
-  double *nxt = acc + FusedCfg<MAT>::SM_ACC;                             // [node][5 kinds][9]
-  for (int t = threadIdx.x; t < 192; t += blockDim.x) sdN[(t / 24) * 25 + t % 24] = (&c_dN[0][0][0])[t];
-  for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_ACC; t += blockDim.x) acc[t] = 0.0;
-  for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_NEXT; t += blockDim.x) nxt[t] = 0.0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = lane >> 3, ia = lane & 7;
-  double *V = jac2_sm + CF::SM_DN + CF::SM_XU + w * CF::VW;
-  double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;
-  const int nxc = NX - 1, nyc = NY - 1, nzc = NZ - 1;
-  const int mx = (nxc + kFT - 1) / kFT;
-  const int tx = blockIdx.x % mx, ty = blockIdx.x / mx;
-  const int i0 = tx * kFT, j0 = ty * kFT;
-  const int64_t nxy = (int64_t)NX * NY;
-  const int64_t n_lines = (int64_t)(mx - 1) * NY + (int64_t)(((nyc + kFT - 1) / kFT) - 1) * NX;
-
-  // write node plane `pk` of the column: interior nodes -> GRID3, side-face nodes -> partial slot
-  auto emit = [&](int pk, int kinds) {
-    for (int t = threadIdx.x; t < kFNodes * 126; t += blockDim.x) {
-      const int node = t % kFNodes, ke = t / kFNodes, kind = ke / 9;
-      const int li = node % kFN, lj = node / kFN, i = i0 + li, j = j0 + lj;
-      if (i >= NX || j >= NY || kind >= kinds) continue;
-      if (edge_line(i, j, NX, NY) >= 0) continue;
-      const int64_t n = i + (int64_t)NX * j + nxy * pk;
-      grid[grid_idx(kind, ke % 9, n, gnpad)] = acc[node * kFAcc + ke];
-    }
-    for (int node = w; node < kFNodes; node += kJac2Warps) {  // warp per side-face node
-      const int li = node % kFN, lj = node / kFN, i = i0 + li, j = j0 + lj;
-      if (i >= NX || j >= NY) continue;
-      const int64_t line = edge_line(i, j, NX, NY);
-      if (line < 0) continue;
-      const int slot = ((li == 0 && i % kFT == 0 && i > 0) ? 1 : 0) + ((lj == 0 && j % kFT == 0 && j > 0) ? 2 : 0);
-      double *o = part + (((int64_t)pk * n_lines + line) * 4 + slot) * 126;
-      for (int ke = lane; ke < 126; ke += 32) o[ke] = (ke / 9 < kinds) ? acc[node * kFAcc + ke] : 0.0;
-    }
-  };
-
-  for (int k = 0; k < nzc; ++k) {
-#pragma unroll 1
-    for (int color = 0; color < 4; ++color) {
-      const int ci = (color & 1) + 2 * c, cj = (color >> 1) + 2 * w;
-      const int gx = i0 + ci, gy = j0 + cj;
-      const bool valid = gx < nxc && gy < nyc;
-      const int64_t e = valid ? gx + (int64_t)nxc * (gy + (int64_t)nyc * k) : 0;
-      double K[5][9];
-      jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
-      if (valid) {
-#pragma unroll
-        for (int d = 0; d < 5; ++d) {
-          if (d == 4 && ia >= 4) break;
-          const int b = (ia + d) & 7;
-          // VTK vertex positions (mesh.py:159-167): a = lz*4 + {0:(0,0),1:(1,0),2:(1,1),3:(0,1)}
-          const int ax = ((ia & 3) == 1 || (ia & 3) == 2), ay = ((ia & 3) >= 2), az = ia >> 2;
-          const int bx = ((b & 3) == 1 || (b & 3) == 2), by = ((b & 3) >= 2), bz = b >> 2;
-          // owner = the lower node id (lexicographic z, y, x); the block of (owner, other)
-          const bool a_owns = (az != bz) ? az < bz : (ay != by) ? ay < by : ax <= bx;
-          const int ox = a_owns ? ax : bx, oy = a_owns ? ay : by, oz = a_owns ? az : bz;
-          const int kind = grid_index(a_owns ? bx - ax : ax - bx, a_owns ? by - ay : ay - by,
-                                      a_owns ? bz - az : az - bz);
-          const int node = (ci + ox) + kFN * (cj + oy);
-          double *dst = (oz == 0) ? acc + node * kFAcc + kind * 9 : nxt + node * kFNext + kind * 9;
-#pragma unroll
-          for (int ii = 0; ii < 3; ++ii)
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk) dst[ii * 3 + kk] += a_owns ? K[d][ii * 3 + kk] : K[d][kk * 3 + ii];
-        }
-      }
-      __syncthreads();  // colour order: every node block sums its cells in a fixed order
-    }
-    emit(k, 14);
-    __syncthreads();
-    for (int t = threadIdx.x; t < kFNodes * 126; t += blockDim.x) {  // plane k+1: carry in, rest zero
-      const int node = t / 126, ke = t % 126;
-      acc[node * kFAcc + ke] = ke < kFNext ? nxt[node * kFNext + ke] : 0.0;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < FusedCfg<MAT>::SM_NEXT; t += blockDim.x) nxt[t] = 0.0;
-    __syncthreads();
-  }
-  emit(nzc, 5);  // the top plane: in-plane blocks from the last layer only
-}
-
-// side-face nodes: GRID3 block = sum of the columns' partial blocks in slot order (fixed)
-__global__ void __launch_bounds__(kThreads) k_grid_edge_finish(int NX, int NY, int NZ, int64_t gnpad,
-                                                               const double *__restrict__ part,
-                                                               double *__restrict__ grid) {
-  const int nxc = NX - 1, nyc = NY - 1;
-  const int mx = (nxc + kFT - 1) / kFT, my = (nyc + kFT - 1) / kFT;
-  const int64_t n_lines = (int64_t)(mx - 1) * NY + (int64_t)(my - 1) * NX;
-  const int64_t total = n_lines * NZ * 126;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int ke = (int)(t % 126);
-    const int64_t lp = t / 126, line = lp % n_lines, pk = lp / n_lines;
-    int i, j;
-    if (line < (int64_t)(mx - 1) * NY) {
-      i = (int)(line / NY + 1) * kFT;
-      j = (int)(line % NY);
-    } else {
-      const int64_t r = line - (int64_t)(mx - 1) * NY;
-      j = (int)(r / NX + 1) * kFT;
-      i = (int)(r % NX);
-    }
-    if (edge_line(i, j, NX, NY) != line) continue;  // a y-line slot of an x-line node: unused
-    const bool xe = i % kFT == 0 && i > 0 && i < nxc, ye = j % kFT == 0 && j > 0 && j < nyc;
-    const double *p = part + ((pk * n_lines + line) * 4) * 126 + ke;
-    double v = p[0];
-    if (xe) v += p[126];
-    if (ye) v += p[2 * 126];
-    if (xe && ye) v += p[3 * 126];
-    grid[grid_idx(ke / 9, ke % 9, i + (int64_t)NX * j + (int64_t)NX * NY * pk, gnpad)] = v;
-  }
-}
-
-static int64_t fused_part_doubles(int NX, int NY, int NZ) {
-  const int mx = (NX - 1 + kFT - 1) / kFT, my = (NY - 1 + kFT - 1) / kFT;
-  return ((int64_t)(mx - 1) * NY + (int64_t)(my - 1) * NX) * NZ * 4 * 126;
-}
-
-template <int MAT>
-static void launch_fused(Ctx *c, cudaStream_t s, const ElemArgs &a, double *grid) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tangent_grid_fused<MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)FusedCfg<MAT>::BYTES);
-    attr = true;
-  }
-  const int mx = (c->grid_nx - 1 + kFT - 1) / kFT, my = (c->grid_ny - 1 + kFT - 1) / kFT;
-  k_tangent_grid_fused<MAT><<<mx * my, kJac2Warps * 32, FusedCfg<MAT>::BYTES, s>>>(
-      a, c->grid_nx, c->grid_ny, c->grid_nz, c->grid_npad, grid, c->scratch);
-  const int64_t total = fused_part_doubles(c->grid_nx, c->grid_ny, c->grid_nz) / 4;
-  if (total > 0)
-    k_grid_edge_finish<<<grid_cap(total, kThreads), kThreads, 0, s>>>(c->grid_nx, c->grid_ny, c->grid_nz,
-                                                                     c->grid_npad, c->scratch, grid);
-  count_launch(2);
-}
-
 template <int MAT>
 static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, double *Ke, int soa) {
   static bool attr = false;  // > 48 KB of shared memory is opt-in per kernel
@@ -1757,15 +1577,15 @@ static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, dou
   k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
 }
 
-// B200FEM_TANGENT = v2 (default: node-lane phase A) | v1 (pair-per-lane phase A) | fused
-// (lattice column kernel for the GRID3 tangent, v2 elsewhere: correct, but one 200 KB CTA of 4
-// warps per SM leaves it latency bound -- 16.0 ms against 8.4 ms for v2 + pull at config 3,
-// profiles/r02_tangent_ab.jsonl).  Read once per process.
+// B200FEM_TANGENT = v2 (default: node-lane phase A) | v1 (the r01 pair-per-lane phase A, kept as
+// the A/B reference of tools/tangent_ab.py).  A fused lattice column kernel without the per-cell
+// scratch was measured at 16.0 ms against 7.1 ms for v2 + pull (one 200 KB CTA of 4 warps per
+// SM: latency bound) and removed (profiles/r02_tangent_ab.jsonl).  Read once per process.
 static int tangent_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("B200FEM_TANGENT");
-    v = !e ? 1 : !strcmp(e, "v1") ? 0 : !strcmp(e, "fused") ? 2 : 1;
+    v = (e && !strcmp(e, "v1")) ? 0 : 1;
   }
   return v;
 }
@@ -1779,20 +1599,6 @@ int launch_jacobian(Ctx *c, const double *U, double *data, b200fem_error *err, d
   // (element-major scratch for vec 1; vec 3 keeps the cell-major blocks, whose 72-byte rows the
   // pull reads whole -- element-major stores of a warp-per-cell kernel would be partial sectors)
   const bool pull = grid && !data && !sym && c->grid_nx && !getenv("B200FEM_NO_GRID_PULL");
-  if (pull && c->vec == 3 && tangent_variant() == 2 && c->grid_nx > 1 && c->grid_ny > 1 && c->grid_nz > 1) {
-    // fused column kernel: no per-cell scratch (the scratch holds the side-face partials)
-    if (ensure_scratch(c, (size_t)std::max<int64_t>(1, fused_part_doubles(c->grid_nx, c->grid_ny, c->grid_nz)),
-                       err))
-      return B200FEM_E_CUDA;
-    const ElemArgs a2 = make_args(c, U);
-    switch (c->material) {
-      case B200FEM_MAT_LE: launch_fused<B200FEM_MAT_LE>(c, s, a2, grid); break;
-      case B200FEM_MAT_NH: launch_fused<B200FEM_MAT_NH>(c, s, a2, grid); break;
-      default: launch_fused<B200FEM_MAT_J2>(c, s, a2, grid); break;
-    }
-    B200_CUDA_E(cudaGetLastError(), err);
-    return fetch_element_errors(c, err, true);
-  }
   if (ensure_scratch(c, (size_t)c->n_cells * 36 * vv, err)) return B200FEM_E_CUDA;
   const ElemArgs a = make_args(c, U);
   // reference CSR layout on a scalar lattice: the same pull (assemble_jacobian, operator="csr").

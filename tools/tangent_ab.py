@@ -3,7 +3,6 @@
     python tools/tangent_ab.py [--n 136] [--reps 5]
 
 Runs one subprocess per variant (the switches are read once per process):
-  fused : B200FEM_TANGENT=fused -> k_tangent_grid_fused + k_grid_edge_finish
   v2    : B200FEM_TANGENT=v2    -> k_jacobian_v2 (node-lane phase A) + k_grid_pull
   v1    : B200FEM_TANGENT=v1    -> k_jacobian (pair-per-lane phase A) + k_grid_pull
 Each times ws.jacobian_grid at a perturbed U (CUDA events, after warm-up), the residual, and
@@ -55,8 +54,7 @@ np.save(out, D.to_host(G.matvec(x)))
 print(json.dumps({"jacobian_s": t_jac, "residual_s": t_res, "n_cells": prob.mesh.n_cells}))
 '''
 
-VARIANTS = {"fused": {"B200FEM_TANGENT": "fused"}, "v2": {"B200FEM_TANGENT": "v2"},
-            "v1": {"B200FEM_TANGENT": "v1"}}
+VARIANTS = {"v2": {"B200FEM_TANGENT": "v2"}, "v1": {"B200FEM_TANGENT": "v1"}}
 
 
 def main():
