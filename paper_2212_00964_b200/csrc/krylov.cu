@@ -73,81 +73,6 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
   if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0 && inline_stage) apply_stage(ST_XR, S, tot);
 }
 
-// ---- "split" iteration: plain SpMVs (y1 = A p, y2 = A s) and the Jacobi scaling v = D^-1 y1,
-// t = D^-1 y2 applied by the streaming kernels that read them.  The GRID3 matvec then runs in its
-// plain mode (460 us at config 3) instead of the Jacobi modes (~530 us: the two extra row
-// operands cost it registers and L2 capacity), at the price of one streaming dot pass per matvec.
-// Same recurrence and scalar stages as enqueue_iteration; y1, y2 live in w->v, w->t.
-__global__ void __launch_bounds__(kThreads) k_update_p_split(int64_t n, const double *__restrict__ r,
-                                                             const double *__restrict__ y1,
-                                                             const double *__restrict__ inv, double *__restrict__ p,
-                                                             const KrylovScalars *S) {
-  if (S->status != KS_RUNNING) return;
-  const double beta = S->beta, omega = S->omega;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = r[i] + beta * (p[i] - omega * (inv[i] * y1[i]));
-}
-
-// r0 . (D^-1 y1) -> alpha (ST_R0)
-__global__ void __launch_bounds__(kThreads) k_dot_r0v(int64_t n, const double *__restrict__ y1,
-                                                      const double *__restrict__ inv, const double *__restrict__ r0,
-                                                      KrylovScalars *S, RedScratch red) {
-  if (S->status != KS_RUNNING) return;
-  double acc[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    acc[0] = fma(r0[i], inv[i] * y1[i], acc[0]);
-  double tot[1];
-  if (block_partials_and_finish<1>(acc, red, tot) && threadIdx.x == 0) apply_stage(ST_R0, S, tot);
-}
-
-__global__ void __launch_bounds__(kThreads) k_update_s_split(int64_t n, const double *__restrict__ r,
-                                                             const double *__restrict__ y1,
-                                                             const double *__restrict__ inv, double *__restrict__ s,
-                                                             const KrylovScalars *S) {
-  if (S->status != KS_RUNNING) return;
-  const double alpha = S->alpha;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    s[i] = r[i] - alpha * (inv[i] * y1[i]);
-}
-
-// t = D^-1 y2: t.t, t.s -> omega (ST_TT)
-__global__ void __launch_bounds__(kThreads) k_dot_tt(int64_t n, const double *__restrict__ y2,
-                                                     const double *__restrict__ inv, const double *__restrict__ s,
-                                                     KrylovScalars *S, RedScratch red) {
-  if (S->status != KS_RUNNING) return;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double t = inv[i] * y2[i];
-    acc[0] = fma(t, t, acc[0]);
-    acc[1] = fma(t, s[i], acc[1]);
-  }
-  double tot[2];
-  if (block_partials_and_finish<2>(acc, red, tot) && threadIdx.x == 0) apply_stage(ST_TT, S, tot);
-}
-
-__global__ void __launch_bounds__(kThreads) k_update_xr_split(int64_t n, double *__restrict__ x, double *__restrict__ r,
-                                                              const double *__restrict__ p, const double *__restrict__ s,
-                                                              const double *__restrict__ y2,
-                                                              const double *__restrict__ inv,
-                                                              const double *__restrict__ r0,
-                                                              const double *__restrict__ dg, KrylovScalars *S,
-                                                              RedScratch red) {
-  if (S->status != KS_RUNNING) return;
-  const double alpha = S->alpha, omega = S->omega;
-  double acc[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += alpha * p[i] + omega * s[i];
-    const double ri = s[i] - omega * (inv[i] * y2[i]);
-    r[i] = ri;
-    const double dr = dg[i] * ri;
-    acc[0] = fma(dr, dr, acc[0]);
-    acc[1] = fma(r0[i], ri, acc[1]);
-    acc[2] = fma(ri, ri, acc[2]);
-  }
-  double tot[3];
-  if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0) apply_stage(ST_XR, S, tot);
-}
-
 // ---------------------------------------------------------------- Jacobi-PCG
 // For symmetric operators (Poisson, LE, NH, SIMP, J2 tangents; BASELINE config 2 "linear
 // assembly + PCG").  The Dirichlet rows of the assembled K are identity rows, so starting
@@ -304,35 +229,7 @@ static int run_loop_graph(Matrix *m, LoopGraph &lg, F &&enqueue, b200fem_error *
 
 static int grid_vec(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
 
-// B200FEM_BICG_SPLIT=1: the split iteration (A/B)
-static bool bicg_split() {
-  static int v = -1;
-  if (v < 0) v = getenv("B200FEM_BICG_SPLIT") ? 1 : 0;
-  return v == 1;
-}
-
-static void enqueue_iteration_split(Matrix *m, double *x) {
-  KrylovWork *w = m->kw;
-  cudaStream_t s = m->stream;
-  const int64_t n = m->n;
-  k_update_p_split<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->inv, w->p, w->sc);
-  SpmvArgs a1{w->p, w->v, nullptr, nullptr, nullptr, nullptr, w->sc, 0};
-  launch_spmv(m, SP_PLAIN, a1, nullptr);
-  k_dot_r0v<<<kRedBlocks, kThreads, 0, s>>>(n, w->v, w->inv, w->r0, w->sc, w->red);
-  k_update_s_split<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->inv, w->s, w->sc);
-  SpmvArgs a2{w->s, w->t, nullptr, nullptr, nullptr, nullptr, w->sc, 0};
-  launch_spmv(m, SP_PLAIN, a2, nullptr);
-  k_dot_tt<<<kRedBlocks, kThreads, 0, s>>>(n, w->t, w->inv, w->s, w->sc, w->red);
-  k_update_xr_split<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->inv, w->r0, w->diag, w->sc,
-                                                    w->red);
-  count_launch(5);
-}
-
 static void enqueue_iteration(Matrix *m, const double *b, double *x) {
-  if (bicg_split()) {
-    enqueue_iteration_split(m, x);
-    return;
-  }
   KrylovWork *w = m->kw;
   cudaStream_t s = m->stream;
   const int64_t n = m->n;
@@ -501,7 +398,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
       if (int rc = run_loop_graph(m, loop_graph, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
       B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
       B200_CUDA_E(cudaStreamSynchronize(s), err);
-      count_launch((bicg_split() ? 7 : 5) * (H[1].it - it0) + 1);
+      count_launch(5 * (H[1].it - it0) + 1);
       cur = 1;  // the snapshot is in H[1 + (cur ^ 1)]
     } else {
       int batch = 4;
