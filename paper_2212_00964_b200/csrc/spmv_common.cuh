@@ -42,13 +42,13 @@ __device__ __forceinline__ void spmv_epilogue(int64_t i, double acc, const SpmvA
                                               double &red0, double &red1) {
   if (MODE == SP_PLAIN) {
     a.y[i] = acc;
-  } else if (MODE == SP_JACOBI_R0) {
-    const double v = p.inv * acc;
-    a.y[i] = v;
+  } else if (MODE == SP_JACOBI_R0) {  // v, t: streaming stores (consumed by the vector kernels
+    const double v = p.inv * acc;    // after the whole matrix has streamed through L2)
+    __stcs(a.y + i, v);
     red0 = fma(p.aux, v, red0);
   } else if (MODE == SP_JACOBI_TT) {
     const double t = p.inv * acc;
-    a.y[i] = t;
+    __stcs(a.y + i, t);
     red0 = fma(t, t, red0);
     red1 = fma(t, p.xi, red1);
   } else if (MODE == SP_RESIDUAL) {
