@@ -73,89 +73,6 @@ __global__ void __launch_bounds__(kThreads) k_update_xr(int64_t n, double *__res
   if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0 && inline_stage) apply_stage(ST_XR, S, tot);
 }
 
-// 16-byte (double2) variants of the three BiCGSTAB vector kernels: half the load / store
-// instructions per byte (k_update_xr streams 8 vectors at 5.0 TB/s in the scalar form).
-// Used when every pointer is 16-byte aligned (single-GPU solves; partition slices may not be);
-// an odd tail element is handled by the last pair's thread.
-__global__ void __launch_bounds__(kThreads) k_update_p2(int64_t n, const double *__restrict__ r,
-                                                        const double *__restrict__ v, double *__restrict__ p,
-                                                        const KrylovScalars *S) {
-  if (S->status != KS_RUNNING) return;
-  const double beta = S->beta, omega = S->omega;
-  const int64_t n2 = (n + 1) >> 1;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n2; j += (int64_t)gridDim.x * blockDim.x) {
-    if (2 * j + 1 < n) {
-      const double2 rr = reinterpret_cast<const double2 *>(r)[j], vv = reinterpret_cast<const double2 *>(v)[j];
-      double2 pp = reinterpret_cast<double2 *>(p)[j];
-      pp.x = rr.x + beta * (pp.x - omega * vv.x);
-      pp.y = rr.y + beta * (pp.y - omega * vv.y);
-      reinterpret_cast<double2 *>(p)[j] = pp;
-    } else {
-      p[2 * j] = r[2 * j] + beta * (p[2 * j] - omega * v[2 * j]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_update_s2(int64_t n, const double *__restrict__ r,
-                                                        const double *__restrict__ v, double *__restrict__ s,
-                                                        const KrylovScalars *S) {
-  if (S->status != KS_RUNNING) return;
-  const double alpha = S->alpha;
-  const int64_t n2 = (n + 1) >> 1;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n2; j += (int64_t)gridDim.x * blockDim.x) {
-    if (2 * j + 1 < n) {
-      const double2 rr = reinterpret_cast<const double2 *>(r)[j], vv = reinterpret_cast<const double2 *>(v)[j];
-      reinterpret_cast<double2 *>(s)[j] = make_double2(rr.x - alpha * vv.x, rr.y - alpha * vv.y);
-    } else {
-      s[2 * j] = r[2 * j] - alpha * v[2 * j];
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_update_xr2(int64_t n, double *__restrict__ x, double *__restrict__ r,
-                                                         const double *__restrict__ p, const double *__restrict__ s,
-                                                         const double *__restrict__ t, const double *__restrict__ r0,
-                                                         const double *__restrict__ dg, KrylovScalars *S,
-                                                         RedScratch red) {
-  if (S->status != KS_RUNNING) return;
-  const double alpha = S->alpha, omega = S->omega;
-  double acc[3] = {0.0, 0.0, 0.0};
-  const int64_t n2 = (n + 1) >> 1;
-  auto one = [&](double &xi, double pi, double si, double ti, double r0i, double dgi, double &ri) {
-    xi += alpha * pi + omega * si;
-    ri = si - omega * ti;
-    const double dr = dgi * ri;
-    acc[0] = fma(dr, dr, acc[0]);
-    acc[1] = fma(r0i, ri, acc[1]);
-    acc[2] = fma(ri, ri, acc[2]);
-  };
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n2; j += (int64_t)gridDim.x * blockDim.x) {
-    if (2 * j + 1 < n) {
-      double2 xx = reinterpret_cast<double2 *>(x)[j];
-      const double2 pp = reinterpret_cast<const double2 *>(p)[j], ss = reinterpret_cast<const double2 *>(s)[j],
-                    tt = reinterpret_cast<const double2 *>(t)[j], qq = reinterpret_cast<const double2 *>(r0)[j],
-                    dd = reinterpret_cast<const double2 *>(dg)[j];
-      double2 rr;
-      one(xx.x, pp.x, ss.x, tt.x, qq.x, dd.x, rr.x);
-      one(xx.y, pp.y, ss.y, tt.y, qq.y, dd.y, rr.y);
-      reinterpret_cast<double2 *>(x)[j] = xx;
-      reinterpret_cast<double2 *>(r)[j] = rr;
-    } else {
-      const int64_t i = 2 * j;
-      one(x[i], p[i], s[i], t[i], r0[i], dg[i], r[i]);
-    }
-  }
-  double tot[3];
-  if (block_partials_and_finish<3>(acc, red, tot) && threadIdx.x == 0) apply_stage(ST_XR, S, tot);
-}
-
-static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
-static bool vec2_kernels() {
-  static int v = -1;
-  if (v < 0) v = getenv("B200FEM_VEC_SCALAR") ? 0 : 1;  // A/B switch: scalar vector kernels
-  return v == 1;
-}
-
 // ---------------------------------------------------------------- Jacobi-PCG
 // For symmetric operators (Poisson, LE, NH, SIMP, J2 tangents; BASELINE config 2 "linear
 // assembly + PCG").  The Dirichlet rows of the assembled K are identity rows, so starting
@@ -316,17 +233,13 @@ static void enqueue_iteration(Matrix *m, const double *b, double *x) {
   KrylovWork *w = m->kw;
   cudaStream_t s = m->stream;
   const int64_t n = m->n;
-  const bool v2 = vec2_kernels() && aligned16(x);  // the work vectors are cudaMalloc'ed
-  if (v2) k_update_p2<<<grid_vec((n + 1) / 2), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
-  else k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
+  k_update_p<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->p, w->sc);
   SpmvArgs a1{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 1};
   launch_spmv(m, SP_JACOBI_R0, a1, &w->red);
-  if (v2) k_update_s2<<<grid_vec((n + 1) / 2), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
-  else k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
+  k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
   SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 1};
   launch_spmv(m, SP_JACOBI_TT, a2, &w->red);
-  if (v2) k_update_xr2<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red);
-  else k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
+  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
   count_launch(3);
   (void)b;
 }
