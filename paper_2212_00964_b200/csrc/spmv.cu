@@ -530,6 +530,107 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
   }
 }
 
+template <int MODE, typename VT>
+__global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : kGMinBlocks) k_spmv_grid3_pf(const VT *__restrict__ grid, GridDims g,
+                                                             const uint8_t *__restrict__ dir_flag, int node_lo,
+                                                             int node_hi, SpmvArgs a, RedScratch red) {
+  if (a.sc && a.sc->status != KS_RUNNING) return;
+  // Row operands of the epilogue, software-pipelined one chunk ahead: while chunk i is computed,
+  // each lane's cp.async copies of ITS OWN three rows of chunk i+1 are in flight into its private
+  // shared-memory slots (no registers held, no cross-lane dependency, no __syncwarp); the
+  // epilogue of chunk i waits only for the group issued during chunk i-1.
+  constexpr int NE = n_ext<MODE>();
+  __shared__ double s_pf[2][NE > 0 ? NE : 1][kGThreads * 3];
+  const int lane = threadIdx.x & 31;
+  const int warp0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int64_t np = g.npad;
+  double red0 = 0.0, red1 = 0.0;
+  const int nch = (int)(np >> 5);
+  const SlabWalk sw = slab_walk(g, node_lo, node_hi);
+  auto prefetch = [&](int64_t wn, int buf) {  // this lane's rows of work item wn
+    if (wn < sw.n_work) {
+      int lo2, hi2;
+      const int c2 = sw.chunk(wn, g, node_lo, node_hi, lo2, hi2);
+      const int node2 = (c2 << 5) + lane;
+      if (node2 >= lo2 && node2 < hi2) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const double *src = ext_ptr<MODE>(a, e) + 3 * (int64_t)node2;
+#pragma unroll
+          for (int r = 0; r < 3; ++r) cp_async8(&s_pf[buf][e][3 * threadIdx.x + r], src + r);
+        }
+      }
+    }
+    cp_async_commit();  // one group per work item (possibly empty)
+  };
+  if (NE > 0) prefetch(warp0, 0);
+  int buf = 0;
+  for (int64_t w = warp0; w < sw.n_work; w += nwarps, buf ^= 1) {
+    if (NE > 0) prefetch(w + nwarps, buf ^ 1);
+    int lo, hi;
+    const int c = sw.chunk(w, g, node_lo, node_hi, lo, hi);
+    const int c0 = c << 5, node = c0 + lane;
+    if (node < lo || node >= hi) continue;
+    const LatticePos p = lattice_pos(node, c0, g);
+    const double *__restrict__ x = a.x;
+    // the epilogue's row operands (D^-1, r0 / b / x_i, Dirichlet flags) are loaded first so
+    // their latency hides behind the 27 block products instead of trailing them
+    bool dfl[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) dfl[r] = dir_flag && __ldg(dir_flag + 3 * (int64_t)node + r);
+    double yu[3] = {0.0, 0.0, 0.0}, yl[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {  // upper: B_q[a] x_{a + off_q}
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, di, dj, dk);
+      const int m = node + di + dj * g.nx + dk * g.nxy;
+      VT b[9];
+      double xm[3];
+      grid_block(grid, (int64_t)q * nch + c, lane, ok, b);  // first use: normal L2 policy
+#pragma unroll
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        yu[r] = fma((double)b[3 * r + 2], xm[2], fma((double)b[3 * r + 1], xm[1], fma((double)b[3 * r], xm[0], yu[r])));
+    }
+#pragma unroll
+    // lower: B_q[a - off_q]^T x_{a - off_q}.  Normal L2 policy, not evict-first: the warp
+    // streaming node a - off_q as an upper block runs concurrently in the same wave, so this
+    // read may come first; an evict-first line would then be dropped before that second use
+    // (ncu DRAM 2.81 -> 2.73 GB, 474 -> 463 us per matvec at config 3).
+    for (int q = 1; q < 14; ++q) {
+      const int di = grid_di(q), dj = grid_dj(q), dk = grid_dk(q);
+      const bool ok = grid_has(p, -di, -dj, -dk);
+      const int m = node - di - dj * g.nx - dk * g.nxy;
+      VT b[9];
+      double xm[3];
+      grid_block(grid, (int64_t)q * nch + (m >> 5), m & 31, ok, b);  // normal policy (see below)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) xm[t] = ok ? __ldg(x + 3 * (int64_t)m + t) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        yl[r] = fma((double)b[6 + r], xm[2], fma((double)b[3 + r], xm[1], fma((double)b[r], xm[0], yl[r])));
+    }
+    if (NE > 0) cp_async_wait_1();  // this item's rows (issued one item ago) have landed
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int64_t row = 3 * (int64_t)node + r;
+      const double acc = dfl[r] ? __ldg(x + row) : yu[r] + yl[r];
+      const int t = 3 * threadIdx.x + r;
+      const RowPre pre = row_pre_from<MODE>(&s_pf[buf][0][t], &s_pf[buf][NE > 1 ? 1 : 0][t],
+                                            &s_pf[buf][NE > 2 ? 2 : 0][t]);
+      spmv_epilogue<MODE>(row, acc, a, pre, red0, red1);
+    }
+  }
+  if (NE > 0) cp_async_wait_all();  // no copy may outlive the block
+  if (MODE != SP_PLAIN) {
+    double v2[2] = {red0, red1}, tot[2];
+    if (block_partials_and_finish<2, kGThreads / 32>(v2, red, tot) && threadIdx.x == 0 && a.inline_stage)
+      spmv_stage<MODE>(a.sc, tot);
+  }
+}
+
 // Scalar (vec 1, Poisson) GRID: one value per offset; a thread per node, 4 CTAs per SM.
 template <int MODE>
 __global__ void __launch_bounds__(kGThreads, 4) k_spmv_grid1(const double *__restrict__ grid, GridDims g,
@@ -642,6 +743,13 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   }
 }
 
+// B200FEM_GRID_PREFETCH=1: the row-operand prefetch variant of the Jacobi-mode GRID3 matvec (A/B)
+static bool grid_prefetch() {
+  static int v = -1;
+  if (v < 0) v = getenv("B200FEM_GRID_PREFETCH") ? 1 : 0;
+  return v == 1;
+}
+
 template <int MODE>
 static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
@@ -662,6 +770,8 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
       if (m->data32)
         k_spmv_grid3<MODE, float><<<(int)std::min<int64_t>((int64_t)kGMinBlocks32 * gg, std::max(1, (nch + 7) / 8)),
                                     kGThreads, 0, m->stream>>>(m->data32, g, m->dir_flag, lo, hi, a, r);
+      else if (MODE != SP_PLAIN && grid_prefetch())
+        k_spmv_grid3_pf<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
       else
         k_spmv_grid3<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
     }
