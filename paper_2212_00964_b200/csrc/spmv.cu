@@ -743,10 +743,12 @@ __global__ void __launch_bounds__(kThreads) k_spmv_csr(const int32_t *__restrict
   }
 }
 
-// B200FEM_GRID_PREFETCH=1: the row-operand prefetch variant of the Jacobi-mode GRID3 matvec (A/B)
+// Jacobi / residual modes of the FP64 GRID3 matvec use the row-operand prefetch kernel
+// (504 / 492 us against 511 / 516 us with register preloads, config 3, profiles/r02_grid_prefetch_ab.jsonl);
+// B200FEM_GRID_NO_PREFETCH=1 restores the preload kernel (A/B).
 static bool grid_prefetch() {
   static int v = -1;
-  if (v < 0) v = getenv("B200FEM_GRID_PREFETCH") ? 1 : 0;
+  if (v < 0) v = getenv("B200FEM_GRID_NO_PREFETCH") ? 0 : 1;
   return v == 1;
 }
 
