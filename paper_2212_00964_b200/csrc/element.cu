@@ -743,11 +743,12 @@ __global__ void __launch_bounds__(kJacWarps * 32, 6) k_jacobian(ElemArgs a, int6
 //     (NH: g, h = H g, u = F g; J2: g, y = s g; LE / Poisson: g) into shared memory;
 //  2. lane (c, a) then owns the symmetric pairs (a, (a + d) mod 8), d = 0..3 (and d = 4 for
 //     a < 4): 36 pairs over 8 lanes, 4 or 5 blocks in registers, accumulated over the 8 points.
-//     Per point a lane reads only the partner vectors V_b (9 doubles for NH) -- the operands it
+//     Per point a lane reads only the partner vectors V_b (9 doubles for NH: g, h and
+//     w = c3 h - c2 u formed once per node in step 1) -- the operands it
 //     reuses (V_a, the coefficients) stay in registers -- so shared-memory wavefronts per cell
 //     drop ~3x against the pair-per-lane kernel above (its 858 wavefronts/cell made it
 //     L1-bound, profiles/r01_ncu_jacobian_nh.json).
-// Block algebra (same as above, with w_b = c3 h_b - c2 u_b formed on the fly):
+// Block algebra (same as above; the own -c2 u_a is recovered as w_a - c3 h_a):
 //   NH:  K_ik += c1 d_ik (g_a.g_b) + h_a,i w_b,k - c2 u_a,i h_b,k + c4 h_a,k h_b,i
 //   J2:  K_ik += c1 d_ik (g_a.g_b) + cl g_a,i g_b,k + c1 g_a,k g_b,i + c3 y_a,i y_b,k
 //   LE:  J2 without the y term;  Poisson: c1 (g_a.g_b)
@@ -909,11 +910,13 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
       const double g[3] = {G[k][0], G[k][1], G[k][2]};
 #pragma unroll
       for (int d = 0; d < 3; ++d) Vq[k * NV + d] = g[d];
-      if (MAT == B200FEM_MAT_NH) {  // h = H g (slot 3), u = F g (slot 6)
+      if (MAT == B200FEM_MAT_NH) {  // h = H g (slot 3), w = c3 h - c2 F g (slot 6)
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          Vq[k * NV + 3 + i] = M2[i][0] * g[0] + M2[i][1] * g[1] + M2[i][2] * g[2];
-          Vq[k * NV + 6 + i] = M1[i][0] * g[0] + M1[i][1] * g[1] + M1[i][2] * g[2];
+          const double h = M2[i][0] * g[0] + M2[i][1] * g[1] + M2[i][2] * g[2];
+          const double u = M1[i][0] * g[0] + M1[i][1] * g[1] + M1[i][2] * g[2];
+          Vq[k * NV + 3 + i] = h;
+          Vq[k * NV + 6 + i] = cf[2] * h - cf[1] * u;
         }
       } else if (MAT == B200FEM_MAT_J2) {  // y = s g (slot 3)
 #pragma unroll
@@ -942,7 +945,7 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
     for (int i = 0; i < 3; ++i) {
       if (MAT == B200FEM_MAT_NH) {
         A1[i] = va[3 + i];
-        A2[i] = -c2 * va[6 + i];
+        A2[i] = fma(-c3, va[3 + i], va[6 + i]);  // w_a - c3 h_a = -c2 u_a
         A3[i] = c4 * va[3 + i];
       } else {
         A1[i] = c2 * va[i];  // cl g_a (c2 slot holds cl for LE / J2)
@@ -965,14 +968,11 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
 #pragma unroll
         for (int i = 0; i < 3; ++i) K[d][i * 3 + i] += dg;
         if (MAT == B200FEM_MAT_NH) {
-          double wb[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) wb[k] = c3 * vb[3 + k] - c2 * vb[6 + k];
 #pragma unroll
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-              K[d][i * 3 + k] = fma(A1[i], wb[k], fma(A2[i], vb[3 + k], fma(A3[k], vb[3 + i], K[d][i * 3 + k])));
+              K[d][i * 3 + k] = fma(A1[i], vb[6 + k], fma(A2[i], vb[3 + k], fma(A3[k], vb[3 + i], K[d][i * 3 + k])));
         } else {
 #pragma unroll
           for (int i = 0; i < 3; ++i)
