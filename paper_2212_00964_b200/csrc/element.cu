@@ -967,17 +967,20 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
         const double dg = c1 * gg;
 #pragma unroll
         for (int i = 0; i < 3; ++i) K[d][i * 3 + i] += dg;
+        // the self block (d = 0) is symmetric: its upper triangle only, mirrored after the loop
         if (MAT == B200FEM_MAT_NH) {
 #pragma unroll
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-              K[d][i * 3 + k] = fma(A1[i], vb[6 + k], fma(A2[i], vb[3 + k], fma(A3[k], vb[3 + i], K[d][i * 3 + k])));
+              if (d > 0 || k >= i)
+                K[d][i * 3 + k] = fma(A1[i], vb[6 + k], fma(A2[i], vb[3 + k], fma(A3[k], vb[3 + i], K[d][i * 3 + k])));
         } else {
 #pragma unroll
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
+              if (d == 0 && k < i) continue;
               double t = fma(A1[i], vb[k], fma(A2[k], vb[i], K[d][i * 3 + k]));
               if (MAT == B200FEM_MAT_J2) t = fma(A3[i], vb[3 + k], t);
               K[d][i * 3 + k] = t;
@@ -985,6 +988,12 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
         }
       }
     }
+  }
+  if (VEC == 3) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < i; ++k) K[0][i * 3 + k] = K[0][k * 3 + i];
   }
 }
 
