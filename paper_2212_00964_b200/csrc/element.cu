@@ -187,31 +187,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_residual(ElemArgs a, int64_t n,
   const double *dNq = sdN + q * 25;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // the node data of the next batch is loaded into registers while this batch computes
-  // (grid-stride loop: the dependent cells -> coords / U loads no longer start each batch)
-  double pX[3], pU[VEC], pT = 0.0;
-  auto fetch = [&](int64_t b0) {
-    const int64_t i0 = b0 + slot;
-    const int64_t e0 = i0 < n ? i0 : (b0 < n ? b0 : 0);
-    const int nd = a.cells[e0 * 8 + q];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) pX[d] = a.coords[(int64_t)nd * 3 + d];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) pU[v] = a.U[(int64_t)nd * VEC + v];
-    if (MAT == B200FEM_MAT_POISSON && a.mp.design_source) pT = a.theta[nd];
-  };
-  if (warp0 * 4 < n) fetch(warp0 * 4);
   for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
     const int64_t idx = base + slot;
     const bool valid = idx < n;
     const int64_t e = valid ? idx : base;
+    const int node = a.cells[e * 8 + q];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) sX[w][slot][q][d] = pX[d];
+    for (int d = 0; d < 3; ++d) sX[w][slot][q][d] = a.coords[(int64_t)node * 3 + d];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) sU[w][slot][q][v] = pU[v];
-    if (MAT == B200FEM_MAT_POISSON && a.mp.design_source) sT[w][slot][q] = pT;
+    for (int v = 0; v < VEC; ++v) sU[w][slot][q][v] = a.U[(int64_t)node * VEC + v];
+    if (MAT == B200FEM_MAT_POISSON && a.mp.design_source) sT[w][slot][q] = a.theta[node];
     __syncwarp();
-    if (base + nwarps * 4 < n) fetch(base + nwarps * 4);
     double G[8][3];
     const double jxw = qp_geometry_s(sX[w][slot], dNq, G);
     double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
