@@ -155,6 +155,19 @@ NH_TANGENT_FLOPS_PER_CELL = 8 * 960 + 36 * 8 * 63
 NH_RESIDUAL_FLOPS_PER_CELL = 8 * 770
 
 
+def jacobi_roofline(kprof, bytes_per_launch, peak):
+    """GB/s of the Jacobi-mode matvecs from the iteration profile (kernels timed one by one)."""
+    if not kprof:
+        return None
+    out = {"bytes_per_launch": bytes_per_launch}
+    for k in ("spmv_jacobi_r0", "spmv_jacobi_tt"):
+        us = kprof["kernels_us"].get(k)
+        if us:
+            gbs = bytes_per_launch / (us * 1e-6) / 1e9
+            out[k] = {"launch_us": us, "achieved_gbs": gbs, "frac": gbs / peak}
+    return out
+
+
 def ncu_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as fh:
@@ -409,7 +422,10 @@ def run_ours(args):
                      "frac": achieved / peak, "bytes_per_launch": bytes_alg,
                      "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,
                      "fem3_equiv_gbs": bytes_fem / t_spmv / 1e9,
-                     "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6},
+                     "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6,
+                     # the two modes the BiCGSTAB iteration actually runs (85 % of the solve):
+                     # + D^-1 and r0 (or s) rows read, the Jacobi-scaled vector written
+                     "in_solve_modes": jacobi_roofline(kprof, bytes_alg + 16 * rows, peak) if grid_op else None},
         "newton": {"linear_method": args.linear, "iterations": rep.n_iterations,
                    "phase_s": getattr(rep, "timings", None),
                    "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
