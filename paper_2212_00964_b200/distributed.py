@@ -330,7 +330,7 @@ class PartitionedSolver:
         storage the parts do not have is an error, not a silent substitution."""
         built = "grid" if all(p.grid for p in self.parts) else "csr"
         want = cfg.operator
-        if want == "auto" or want == built or (want == "grid" and built == "grid"):
+        if want in ("auto", built):
             return
         raise ValueError(f'LinearSolveConfig(operator="{want}") is not available on this PartitionedSolver: '
                          f'its parts were built with the "{built}" operator (PartitionedSolver(..., operator=...))')
