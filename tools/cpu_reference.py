@@ -2,6 +2,7 @@
 
     python tools/cpu_reference.py ladder [n ...]       # gradfem (baseline/_ref) NH newton_solve, phase-timed
     python tools/cpu_reference.py port136 [--n 136]     # oracle port at full size + the GPU solve, U compared
+    python tools/cpu_reference.py fullphases [--n 136]  # gradfem at full size: workspace, R, K, 1st BiCGSTAB
 
 ladder: the UNMODIFIED reference package (pip-installed into baseline/_ref, not /root/reference,
 which does not exist on the GPU box) runs the config-3 problem (NH tensile box n^3, 2 %
@@ -211,10 +212,57 @@ def port136(n):
                           "U_norm": float(np.linalg.norm(U_cpu))}), flush=True)
 
 
+def fullphases(n):
+    """The reference package at the FULL config-3 size, phase by phase, inside one lease: its
+    workspace(), one residual, one AD Jacobian and the first Newton step's BiCGSTAB solve (the
+    whole solve -- three Jacobians and ~1750 Krylov iterations, ~77 min -- does not fit one
+    60-minute lease); the Newton solve's time is these measured phases times their counts."""
+    gf = import_gradfem()
+    threads = os.cpu_count()
+    gf.backend.set_num_threads(threads)
+    import fullsize_cases as fc
+    from gradfem.assembly import workspace
+
+    info = host_info()
+    prob = fc.c3(gf, n)
+    out = {"n": n, "host": info, "threads": threads, "kind": "reference package, full size, per phase"}
+    t0 = time.perf_counter()
+    workspace(prob)
+    out["workspace_s"] = time.perf_counter() - t0
+    print(json.dumps(out), flush=True)
+    U = np.zeros(prob.n_dofs)
+    t0 = time.perf_counter()
+    R = gf.assemble_residual(prob, U)
+    out["residual_s"] = time.perf_counter() - t0
+    print(json.dumps(out), flush=True)
+    t0 = time.perf_counter()
+    K = gf.assemble_jacobian(prob, U)
+    out["jacobian_s"] = time.perf_counter() - t0
+    out["jacobian_us_per_cell"] = out["jacobian_s"] / n ** 3 * 1e6
+    print(json.dumps(out), flush=True)
+    pt = PhaseTimer(gf)
+    try:
+        t0 = time.perf_counter()
+        dU = gf.solvers.bicgstab_jacobi(K, -R)
+        out["bicgstab1_s"] = time.perf_counter() - t0
+    finally:
+        pt.restore()
+    out["bicgstab1_matvecs"] = pt.n["matvec"]
+    out["bicgstab1_s_per_matvec"] = out["bicgstab1_s"] / max(pt.n["matvec"], 1)
+    t0 = time.perf_counter()
+    R1 = gf.assemble_residual(prob, U + dU)
+    out["residual2_s"] = time.perf_counter() - t0
+    out["newton_norms_0_1"] = [float(np.linalg.norm(R)), float(np.linalg.norm(R1))]
+    out["peak_rss_gb"] = peak_rss_gb()
+    print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "ladder":
         ladder([int(a) for a in sys.argv[2:]] or [16, 24, 32, 48, 64])
+    elif cmd == "fullphases":
+        fullphases(int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 136)
     elif cmd == "port136":
         port136(int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 136)
     else:
