@@ -1,10 +1,10 @@
 """Residual and CSR-Jacobian assembly on the GPU (reference gradfem/assembly.py:36-300).
 
 ``workspace(problem)`` replaces the reference's host cache (assembly.py:83-145) with a
-device context (csrc/context.cu): geometry check, CSR pattern, scatter positions,
-diagonal slots and the node -> cell lists of the ordered gathers are built on the B200; the Dirichlet table and the
-fixed Neumann / body load vectors are computed here on the host once (north_star: host
-code keeps the Dirichlet handling) and uploaded.
+device context (csrc/context.cu): geometry check, CSR pattern, scatter positions, diagonal
+slots and the node -> cell lists of the ordered gathers are built on the B200; the Dirichlet
+table and the fixed Neumann / body load vectors are computed here on the host once
+(north_star: host code keeps the Dirichlet handling) and uploaded.
 
 ``assemble_residual`` / ``assemble_jacobian`` keep the reference signatures and return
 host arrays for host inputs (drop-in); pass a CUDA tensor U to stay on the device.

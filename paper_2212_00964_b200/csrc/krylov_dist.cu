@@ -174,8 +174,9 @@ struct Dist {
       cudaStream_t ms = m->stream;
       m->stream = P->s2;
       m->row_lo = P->int_lo, m->row_hi = P->int_hi;
-      if (launch_spmv(m, mode, a[p], &P->red_in)) return B200FEM_E_CUDA;
-      m->stream = ms;
+      const int st = launch_spmv(m, mode, a[p], &P->red_in);
+      m->stream = ms;  // restored on every path
+      if (st) return B200FEM_E_CUDA;
       B200_CUDA(cudaEventRecord(P->ev_done, P->s2));
     }
     if (int st = halo(vec)) return st;
