@@ -136,6 +136,13 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def dist_allreduces(world):
+    """Allreduces per partitioned BiCGSTAB iteration: 2 with the fused dot group (on by default
+    from 4 NCCL ranks, krylov_dist.cu dist_fused_dots), else 3."""
+    e = os.environ.get("B200FEM_DIST_FUSED_DOTS", "")
+    return 2 if (e != "0" if e else world >= 4) else 3
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -411,8 +418,9 @@ def run_ours(args):
         "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated box mesh, 2% stretch BCs)",
-        "config": dict(config(n, s), parallelism=f"node-slab partition x{world} (NCCL halo + allreduce)"
-                       if part is not None else "single GPU"),
+        "config": dict(config(n, s), parallelism=(
+            f"node-slab partition x{world} (NCCL halo + {dist_allreduces(world)} allreduces per BiCGSTAB iteration)"
+            if part is not None else "single GPU")),
         "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": {"kernel": ("k_spmv_grid3 (GRID3 symmetric offset-major storage: 14 upper 3x3 blocks per node, "

@@ -281,7 +281,7 @@ __device__ __forceinline__ void iter_start(KrylovScalars *S) {
   S->rho = rho_new;
 }
 
-enum StageKind : int { ST_R0 = 1, ST_TT = 2, ST_RES = 3, ST_XR = 4, ST_PQ = 5, ST_CGRES = 6, ST_CGXR = 7 };
+enum StageKind : int { ST_R0 = 1, ST_TT = 2, ST_RES = 3, ST_XR = 4, ST_PQ = 5, ST_CGRES = 6, ST_CGXR = 7, ST_TT8 = 8, ST_CONV = 9 };
 // Scalar update after a reduction with global totals tot[] (solvers.py:141-167).
 __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const double *tot) {
   if (!S || S->status != KS_RUNNING) return;
@@ -303,6 +303,24 @@ __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const do
     S->res = sqrt(tot[0]);
     S->r0r = tot[1];
     S->rr = tot[2];
+    if (S->res <= S->tol) {
+      S->status = KS_CONV_INNER;
+      return;
+    }
+    iter_start(S);
+  } else if (kind == ST_TT8) {
+    // partitioned BiCGSTAB with two allreduces per iteration (opt-in): the t-group carries
+    // {t.t, t.s, r0.s, r0.t, s.s, |Ds|^2, Ds.Dt, |Dt|^2}; omega as in ST_TT, then the next
+    // r = s - omega t enters only through the recurrences r0.r, r.r, |Dr|^2 (clamped at 0)
+    S->mv += 1;
+    S->tt = tot[0];
+    S->ts = tot[1];
+    const double om = tot[0] > 0.0 ? tot[1] / tot[0] : 0.0;
+    S->omega = om;
+    S->r0r = tot[2] - om * tot[3];
+    S->rr = fmax(tot[4] - 2.0 * om * tot[1] + om * om * tot[0], 0.0);
+    S->res = sqrt(fmax(tot[5] - 2.0 * om * tot[6] + om * om * tot[7], 0.0));
+  } else if (kind == ST_CONV) {  // after the x, r update of the ST_TT8 flow: as the end of ST_XR
     if (S->res <= S->tol) {
       S->status = KS_CONV_INNER;
       return;

@@ -49,6 +49,7 @@ struct Part {
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
   RedScratch red_in{}, red_lo{}, red_hi{};  // partial dot totals of the three launches
+  RedScratch red6{};  // the extra dots of the two-allreduce BiCGSTAB (lazy)
 };
 
 // total of the three partial dot groups, in a fixed order (deterministic)
@@ -88,6 +89,40 @@ __global__ void __launch_bounds__(kThreads) k_dot_owned(const double *__restrict
     v[0] = fma(x[i], y[i], v[0]);
   double tot[1];
   block_partials_and_finish<1>(v, red, tot);
+}
+
+// {r0.s, r0.t, s.s, |Ds|^2, Ds.Dt, |Dt|^2} over the owned rows; totals land in out[0..5]
+__global__ void __launch_bounds__(kThreads) k_dot6(int64_t n, const double *__restrict__ r0,
+                                                   const double *__restrict__ s, const double *__restrict__ t,
+                                                   const double *__restrict__ dg, const KrylovScalars *S,
+                                                   RedScratch red) {
+  if (S->status != KS_RUNNING) return;
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double si = s[i], ti = t[i], qi = r0[i], d = dg[i];
+    const double ds = d * si, dt = d * ti;
+    acc[0] = fma(qi, si, acc[0]);
+    acc[1] = fma(qi, ti, acc[1]);
+    acc[2] = fma(si, si, acc[2]);
+    acc[3] = fma(ds, ds, acc[3]);
+    acc[4] = fma(ds, dt, acc[4]);
+    acc[5] = fma(dt, dt, acc[5]);
+  }
+  double tot[6];
+  block_partials_and_finish<6>(acc, red, tot);
+}
+
+// x += alpha p + omega s, r = s - omega t, without reductions (their dots came by recurrence)
+__global__ void __launch_bounds__(kThreads) k_update_xr_nored(int64_t n, double *__restrict__ x,
+                                                              double *__restrict__ r, const double *__restrict__ p,
+                                                              const double *__restrict__ s,
+                                                              const double *__restrict__ t, const KrylovScalars *S) {
+  if (S->status != KS_RUNNING) return;
+  const double alpha = S->alpha, omega = S->omega;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i] + omega * s[i];
+    r[i] = s[i] - omega * t[i];
+  }
 }
 
 static int grid_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
@@ -265,6 +300,72 @@ static int enqueue_dist_iteration(Dist &D, double *const *x) {
   }
   st |= D.allreduce(3);
   D.stage(ST_XR);
+  return st || cudaPeekAtLastError() != cudaSuccess ? B200FEM_E_CUDA : 0;
+}
+
+// BiCGSTAB iteration with TWO allreduces (opt-in, B200FEM_DIST_FUSED_DOTS=1): the t-group also
+// carries r0.s, r0.t, s.s, |Ds|^2, Ds.Dt, |Dt|^2 (one extra pass over 4 owned vectors), from
+// which ST_TT8 forms omega and the next r's r0.r, r.r, |Dr|^2 by the recurrence r = s - omega t;
+// x and r are then updated without a reduction.  Same iterates in exact arithmetic; in floating
+// point the recurrence norms drift from the explicit ones, so the explicit residual of the
+// outer loop (solvers.py:115-118) still decides convergence.  Pays only when an allreduce's
+// latency exceeds the extra pass: by default on NCCL communicators of >= 4 ranks
+// (DESIGN.md section 5); B200FEM_DIST_FUSED_DOTS=1 / =0 forces it on / off.
+static bool dist_fused_dots(const Dist &D) {
+  const char *e = getenv("B200FEM_DIST_FUSED_DOTS");
+  if (e && *e) return *e != '0';
+  return D.comm->kind == 1 && D.comm->nranks >= 4;
+}
+
+static int enqueue_dist_iteration_fused(Dist &D, double *const *x) {
+  const size_t np = D.parts.size();
+  std::vector<double *> pv(np), sv(np);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_p<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->p + lo, w->sc);
+    count_launch();
+    pv[p] = w->p;
+    sv[p] = w->s;
+  }
+  std::vector<SpmvArgs> a1(np), a2(np);
+  for (size_t p = 0; p < np; ++p) {
+    KrylovWork *w = D.parts[p]->m->kw;
+    a1[p] = SpmvArgs{w->p, w->v, w->inv, w->diag, w->r0, nullptr, w->sc, 0};
+    a2[p] = SpmvArgs{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 0};
+  }
+  int st = D.spmv(SP_JACOBI_R0, a1, pv.data(), 1);
+  st |= D.allreduce(1);
+  D.stage(ST_R0);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_s<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, w->r + lo, w->v + lo, w->s + lo, w->sc);
+    count_launch();
+  }
+  st |= D.spmv(SP_JACOBI_TT, a2, sv.data(), 2);
+  for (size_t p = 0; p < np; ++p) {  // the six extra dots into red.result[2..7]
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    if (!P->red6.partials && red_alloc(&P->red6)) return B200FEM_E_CUDA;
+    RedScratch r6{P->red6.partials, P->red6.ticket, w->red.result + 2};
+    k_dot6<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, w->r0 + lo, w->s + lo, w->t + lo, w->diag + lo, w->sc, r6);
+    count_launch();
+  }
+  st |= D.allreduce(8);
+  D.stage(ST_TT8);
+  for (size_t p = 0; p < np; ++p) {
+    Part *P = D.parts[p];
+    KrylovWork *w = P->m->kw;
+    const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
+    k_update_xr_nored<<<grid_n(n), kThreads, 0, D.stream(p)>>>(n, x[p] + lo, w->r + lo, w->p + lo, w->s + lo,
+                                                               w->t + lo, w->sc);
+    count_launch();
+  }
+  D.stage(ST_CONV);
   return st || cudaPeekAtLastError() != cudaSuccess ? B200FEM_E_CUDA : 0;
 }
 
@@ -489,7 +590,10 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
       k_begin<<<1, 1, 0, D.stream(p)>>>(w->sc);
       count_launch();
     }
-    if (int st = run_batches(D, graph, [&] { return enqueue_dist_iteration(D, x); }, poll, err)) return st;
+    const bool fused = dist_fused_dots(D);
+    if (int st = run_batches(D, graph, [&] { return fused ? enqueue_dist_iteration_fused(D, x)
+                                                           : enqueue_dist_iteration(D, x); }, poll, err))
+      return st;
     it = poll->it;
     mv = poll->mv;
     if (poll->status == KS_BREAKDOWN) {
@@ -695,6 +799,7 @@ int b200fem_part_destroy(b200fem_part *pp) {
   cudaFree(P->recv_nodes);
   cudaFree(P->sendbuf);
   cudaFree(P->recvbuf);
+  if (P->red6.partials) red_free(&P->red6);
   if (P->overlap) {
     cudaStreamSynchronize(P->s2);
     cudaStreamDestroy(P->s2);

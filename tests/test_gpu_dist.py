@@ -158,3 +158,45 @@ print([st.iterations for st in rep.linear_stats])
             outs.append((np.load(f), r.stdout.strip()))
     assert outs[0][1] == outs[1][1]
     assert np.array_equal(outs[0][0], outs[1][0])
+
+
+def test_partitioned_two_allreduce_bicgstab_matches_single_gpu():
+    """B200FEM_DIST_FUSED_DOTS=1: omega and the next r's norms from one fused reduction (2
+    allreduces per iteration instead of 3).  Same Newton solution as the single-GPU solve, and
+    Krylov iteration counts close to the 3-allreduce path's."""
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r'''
+import os, sys, numpy as np
+sys.path[:0] = [os.environ["ROOT"], os.path.join(os.environ["ROOT"], "tests"), os.path.join(os.environ["ROOT"], "tests", "golden")]
+import paper_2212_00964_b200 as fem
+from cases import CASES
+from pkg_cases import build
+from paper_2212_00964_b200.distributed import PartitionedSolver
+_, p, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 10)))
+s = PartitionedSolver(p, nparts=3, mode="local")
+rep = s.newton_solve(cfg=fem.NewtonConfig(rel_tol=1e-10, abs_tol=1e-11),
+                     lin_cfg=fem.LinearSolveConfig(rel_tol=1e-11, abs_tol=1e-13))
+np.save(sys.argv[1], s.gather_U())
+print(sum(st.iterations for st in rep.linear_stats))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    with tempfile.TemporaryDirectory() as d:
+        for fused in (True, False):
+            env = dict(os.environ, ROOT=root)
+            env.pop("B200FEM_DIST_FUSED_DOTS", None)
+            if fused:
+                env["B200FEM_DIST_FUSED_DOTS"] = "1"
+            f = os.path.join(d, f"u{int(fused)}.npy")
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[fused] = (np.load(f), int(r.stdout.strip().splitlines()[-1]))
+    _, p1, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 10)))
+    U1, _ = fem.newton_solve(p1, **TIGHT)
+    for fused in (True, False):
+        U, its = res[fused]
+        assert np.linalg.norm(U - U1) <= 1e-9 * np.linalg.norm(U1), fused
+    assert abs(res[True][1] - res[False][1]) <= max(3, 0.2 * res[False][1])

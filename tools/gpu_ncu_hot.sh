@@ -3,14 +3,14 @@
 cd "$(dirname "$0")/.."
 O=gpurun_out
 export B200FEM_NO_GRAPH=1
-python tools/ncu_targets.py all > $O/c5_targets.log 2>&1 || exit 1
+python tools/ncu_targets.py all > $O/r02b_targets.log 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on -k regex:'k_jacobian_v2|k_grid_pull' -c 2 \
-    -o $O/r02_ncu_tangent python tools/ncu_targets.py tangent > $O/c5_ncu_tangent.log 2>&1
+    -o $O/r02b_ncu_tangent python tools/ncu_targets.py tangent > $O/r02b_ncu_tangent.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'k_residual' -c 2 \
-    -o $O/r02_ncu_residual python tools/ncu_targets.py residual > $O/c5_ncu_residual.log 2>&1
+    -o $O/r02b_ncu_residual python tools/ncu_targets.py residual > $O/r02b_ncu_residual.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'k_spmv_grid3' -c 4 \
-    -o $O/r02_ncu_spmv python tools/ncu_targets.py spmv > $O/c5_ncu_spmv.log 2>&1
+    -o $O/r02b_ncu_spmv python tools/ncu_targets.py spmv > $O/r02b_ncu_spmv.log 2>&1
 for f in tangent residual spmv; do
-  ncu -i $O/r02_ncu_$f.ncu-rep --page raw --csv > $O/r02_ncu_${f}_raw.csv 2>/dev/null
+  ncu -i $O/r02b_ncu_$f.ncu-rep --page raw --csv > $O/r02b_ncu_${f}_raw.csv 2>/dev/null
 done
 ls -la $O
