@@ -17,7 +17,9 @@
 //        it += 1, rho_new = r0.r, breakdown test, beta                   (131-139)
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -321,8 +323,21 @@ static int bicgstab_profile(Matrix *m, const double *b, double *x, int iters, do
   return rc ? B200FEM_E_CUDA : 0;
 }
 
+// B200FEM_KRYLOV_TRACE=1: host timeline of each BiCGSTAB solve on stderr (setup, every
+// restart's explicit residual, every inner loop), for attributing solve time outside the loop.
+static bool krylov_trace() {
+  static int v = -1;
+  if (v < 0) v = getenv("B200FEM_KRYLOV_TRACE") ? 1 : 0;
+  return v == 1;
+}
+static double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, double abs_tol, int64_t max_iters,
              b200fem_solve_info *info, b200fem_error *err) {
+  const bool trace = krylov_trace();
+  const double t_start = trace ? host_ms() : 0.0;
   if (err) memset(err, 0, sizeof(*err)), err->cell = -1, err->qp = -1;
   if (info) memset(info, 0, sizeof(*info));
   if (!(rel_tol > 0) || !(abs_tol > 0)) {
@@ -348,6 +363,7 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
   B200_CUDA_E(cudaStreamSynchronize(s), err);
   const double tol = std::max(rel_tol * std::sqrt(bb), abs_tol);
   const int64_t max_it = max_iters > 0 ? max_iters : 10 * n;
+  if (trace) fprintf(stderr, "[krylov] setup (diagonal, ||b||, sync) %.3f ms\n", host_ms() - t_start);
 
   KrylovScalars *H = w->sc_host;  // [0] control, [1],[2] poll buffers
   memset(H, 0, 3 * sizeof(KrylovScalars));
@@ -366,12 +382,16 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     H[0].mv = mv;
     B200_CUDA_E(cudaMemcpyAsync(w->sc, &H[0], ssz, cudaMemcpyHostToDevice, s), err);
     SpmvArgs ar{x, w->r, w->inv, w->diag, b, w->r0, w->sc, 1};
+    const double t_res = trace ? host_ms() : 0.0;
     if (launch_spmv(m, SP_RESIDUAL, ar, &w->red)) return B200FEM_E_CUDA;
     ++restarts;
     B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
     B200_CUDA_E(cudaStreamSynchronize(s), err);
     mv = H[1].mv;
     const double res = H[1].res;
+    if (trace)
+      fprintf(stderr, "[krylov] restart %lld: explicit residual %.3e (tol %.3e) %.3f ms, total %.3f ms\n", restarts, res,
+              tol, host_ms() - t_res, host_ms() - t_start);
     if (res <= tol) {
       if (info) *info = b200fem_solve_info{it, mv, restarts, res, tol};
       return 0;
@@ -395,10 +415,18 @@ int bicgstab(Matrix *m, const double *b, double *x, int has_x0, double rel_tol, 
     KrylovScalars done{};
     if (use_graph_loop()) {
       const long long it0 = it;
+      const double t_loop = trace ? host_ms() : 0.0;
+      const bool built = loop_graph.exec != nullptr;
       if (int rc = run_loop_graph(m, loop_graph, [&] { enqueue_iteration(m, b, x); }, err)) return rc;
+      const double t_launched = trace ? host_ms() : 0.0;
       B200_CUDA_E(cudaMemcpyAsync(&H[1], w->sc, ssz, cudaMemcpyDeviceToHost, s), err);
       B200_CUDA_E(cudaStreamSynchronize(s), err);
       count_launch(5 * (H[1].it - it0) + 1);
+      if (trace)
+        fprintf(stderr, "[krylov] loop: %lld iterations, status %d, %s+launch %.3f ms, run %.3f ms (%.1f us/it)\n",
+                (long long)(H[1].it - it0), (int)H[1].status, built ? "relaunch" : "capture+instantiate",
+                t_launched - t_loop, host_ms() - t_launched,
+                1e3 * (host_ms() - t_launched) / std::max<long long>(1, H[1].it - it0));
       cur = 1;  // the snapshot is in H[1 + (cur ^ 1)]
     } else {
       int batch = 4;

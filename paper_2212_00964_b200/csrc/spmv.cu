@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
 template <int MODE, typename VT>
 __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : kGMinBlocks) k_spmv_grid3_pf(const VT *__restrict__ grid, GridDims g,
                                                              const uint8_t *__restrict__ dir_flag, int node_lo,
-                                                             int node_hi, SpmvArgs a, RedScratch red) {
+                                                             int node_hi, SpmvArgs a, RedScratch red, int ef) {
   if (a.sc && a.sc->status != KS_RUNNING) return;
   // Row operands of the epilogue, software-pipelined one chunk ahead: while chunk i is computed,
   // each lane's cp.async copies of ITS OWN three rows of chunk i+1 are in flight into its private
@@ -548,6 +548,9 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
   double red0 = 0.0, red1 = 0.0;
   const int nch = (int)(np >> 5);
   const SlabWalk sw = slab_walk(g, node_lo, node_hi);
+  // read-once row operands evict-first, so they do not push out the blocks this matvec
+  // re-reads from L2 (ef = 0: normal policy, the A/B switch B200FEM_GRID_PF_NORMAL=1)
+  const uint64_t pol = l2_evict_first_policy();
   auto prefetch = [&](int64_t wn, int buf) {  // this lane's rows of work item wn
     if (wn < sw.n_work) {
       int lo2, hi2;
@@ -557,8 +560,14 @@ __global__ void __launch_bounds__(kGThreads, sizeof(VT) == 4 ? kGMinBlocks32 : k
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           const double *src = ext_ptr<MODE>(a, e) + 3 * (int64_t)node2;
+          const bool hint = ef && pf_read_once<MODE>(e);
 #pragma unroll
-          for (int r = 0; r < 3; ++r) cp_async8(&s_pf[buf][e][3 * threadIdx.x + r], src + r);
+          for (int r = 0; r < 3; ++r) {
+            if (hint)
+              cp_async8_hint(&s_pf[buf][e][3 * threadIdx.x + r], src + r, pol);
+            else
+              cp_async8(&s_pf[buf][e][3 * threadIdx.x + r], src + r);
+          }
         }
       }
     }
@@ -752,6 +761,12 @@ static bool grid_prefetch() {
   return v == 1;
 }
 
+static int grid_pf_evict_first() {
+  static int v = -1;
+  if (v < 0) v = getenv("B200FEM_GRID_PF_NORMAL") ? 0 : 1;
+  return v;
+}
+
 template <int MODE>
 static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
   const int grid = MODE == SP_PLAIN ? (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (m->n + 63) / 64)) : kRedBlocks;
@@ -773,7 +788,8 @@ static void spmv_dispatch(const Matrix *m, const SpmvArgs &a, RedScratch *red) {
         k_spmv_grid3<MODE, float><<<(int)std::min<int64_t>((int64_t)kGMinBlocks32 * gg, std::max(1, (nch + 7) / 8)),
                                     kGThreads, 0, m->stream>>>(m->data32, g, m->dir_flag, lo, hi, a, r);
       else if (MODE != SP_PLAIN && grid_prefetch())
-        k_spmv_grid3_pf<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
+        k_spmv_grid3_pf<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r,
+                                                                        grid_pf_evict_first());
       else
         k_spmv_grid3<MODE, double><<<gg, kGThreads, 0, m->stream>>>(m->data, g, m->dir_flag, lo, hi, a, r);
     }

@@ -146,6 +146,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy below)
+__device__ __forceinline__ void cp_async8_hint(void *dst, const void *src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -170,6 +180,11 @@ __device__ __forceinline__ const double *ext_ptr(const SpmvArgs &a, int k) {
   if (MODE == SP_RESIDUAL) return k == 0 ? a.inv : (k == 1 ? a.aux : a.dg);
   if (MODE == SP_PQ) return a.x;
   return k == 0 ? a.inv : a.aux;  // SP_CGRES
+}
+// operand e is read once per matvec (not the matvec's own input x, which neighbours re-read)
+template <int MODE>
+__device__ __forceinline__ bool pf_read_once(int k) {
+  return !((MODE == SP_JACOBI_TT && k == 1) || MODE == SP_PQ);
 }
 template <int MODE>
 __device__ __forceinline__ RowPre row_pre_from(const double *e0, const double *e1, const double *e2) {
