@@ -54,8 +54,22 @@ def zeros(n, dtype=None):
     return t.zeros(n, dtype=dtype or t.float64, device=device())
 
 
+_PINNED_MIN_BYTES = 1 << 20
+
+
 def to_host(x) -> np.ndarray:
-    return x.detach().cpu().numpy()
+    """CUDA tensor -> numpy.  Results of 1 MiB or more land in page-locked memory from torch's
+    caching host allocator (the array keeps its tensor alive; the block is reused once the
+    array is dropped): a pinned copy runs at PCIe/C2C speed instead of a pageable staging copy
+    into freshly faulted pages (config-3 U, 62 MB: ~1.5 ms instead of ~15 ms)."""
+    x = x.detach()
+    if not x.is_cuda or x.numel() * x.element_size() < _PINNED_MIN_BYTES:
+        return x.cpu().numpy()
+    t = torch()
+    out = t.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    out.copy_(x, non_blocking=True)
+    t.cuda.current_stream(x.device).synchronize()
+    return out.numpy()
 
 
 def ptr(x):

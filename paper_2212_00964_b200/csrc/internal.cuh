@@ -309,7 +309,7 @@ __device__ __forceinline__ void apply_stage(int kind, KrylovScalars *S, const do
     }
     iter_start(S);
   } else if (kind == ST_TT8) {
-    // partitioned BiCGSTAB with two allreduces per iteration (opt-in): the t-group carries
+    // partitioned BiCGSTAB with two allreduces per iteration (>= 4 NCCL ranks): the t-group carries
     // {t.t, t.s, r0.s, r0.t, s.s, |Ds|^2, Ds.Dt, |Dt|^2}; omega as in ST_TT, then the next
     // r = s - omega t enters only through the recurrences r0.r, r.r, |Dr|^2 (clamped at 0)
     S->mv += 1;
