@@ -101,3 +101,23 @@ def test_nonfinite_u_raises_kernel_evaluation_error_naming_the_element(kind):
         fem.assemble_jacobian(prob, U)
     # the context stays usable after the error
     assert np.all(np.isfinite(fem.assemble_residual(prob, np.zeros(prob.n_dofs))))
+
+
+def test_large_host_results_are_plain_writable_numpy():
+    """Host arrays in give host arrays out: results of >= 1 MiB come back through a pinned
+    buffer (_device.to_host) but are ordinary float64 numpy arrays, equal to the device
+    values, writable, and independent of later solves."""
+    import torch
+
+    from paper_2212_00964_b200 import _device as D
+
+    x = torch.arange(300_000, dtype=torch.float64, device="cuda") * 0.5
+    a = D.to_host(x)
+    b = D.to_host(x[:10])
+    assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (300_000,)
+    assert np.array_equal(a, np.arange(300_000) * 0.5) and np.array_equal(b, a[:10])
+    a[0] = 7.0
+    assert float(x[0]) == 0.0
+    x.fill_(1.0)
+    c = D.to_host(x)
+    assert a[1] == 0.5 and np.all(c == 1.0)
