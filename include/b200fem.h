@@ -241,7 +241,9 @@ int b200fem_part_destroy(b200fem_part *part);
 /* BiCGSTAB over all parts (solvers.py:87-167 semantics, global tolerances and counters);
  * b[p], x[p] are the parts' local device vectors (owned entries are the unknowns).  Batches of
  * iterations run as one captured CUDA graph (kernels + NCCL halo / allreduce) when the parts
- * share a stream; B200FEM_NO_GRAPH=1 enqueues them eagerly. */
+ * share a stream; B200FEM_NO_GRAPH=1 enqueues them eagerly.  Three allreduces per iteration,
+ * two (one fused dot group) on NCCL communicators of >= 4 ranks or with
+ * B200FEM_DIST_FUSED_DOTS=1 (=0 forces three); the explicit residual decides convergence. */
 int b200fem_dist_bicgstab(b200fem_part **parts, int32_t nparts, b200fem_comm *comm, double *const *b,
                           double *const *x, int32_t has_x0, double rel_tol, double abs_tol, int64_t max_iters,
                           b200fem_solve_info *info, b200fem_error *err);
