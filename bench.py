@@ -25,6 +25,7 @@ import tempfile
 import time
 
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # BLAS oversubscription
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # no "NCCL version" banner on stdout next to the JSON line
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -162,16 +163,20 @@ NH_TANGENT_FLOPS_PER_CELL = 8 * 960 + 36 * 8 * 63
 NH_RESIDUAL_FLOPS_PER_CELL = 8 * 770
 
 
-def jacobi_roofline(kprof, bytes_per_launch, peak):
-    """GB/s of the Jacobi-mode matvecs from the iteration profile (kernels timed one by one)."""
+def jacobi_roofline(kprof, plain_bytes, rows, peak):
+    """GB/s of the two Jacobi-mode matvecs the BiCGSTAB iteration runs (k_spmv_grid3_pf, 85 % of
+    the bench step's kernel time), from the iteration profile (kernels timed one by one).
+    Algorithmic bytes over the plain matvec: v = D^-1 A p reads D^-1 and r0 (r0.v), 16 B per row;
+    t = D^-1 A s reads D^-1, 8 B per row (its t.s operand s is the matvec's own input)."""
     if not kprof:
         return None
-    out = {"bytes_per_launch": bytes_per_launch}
-    for k in ("spmv_jacobi_r0", "spmv_jacobi_tt"):
+    out = {}
+    for k, extra in (("spmv_jacobi_r0", 16), ("spmv_jacobi_tt", 8)):
         us = kprof["kernels_us"].get(k)
         if us:
-            gbs = bytes_per_launch / (us * 1e-6) / 1e9
-            out[k] = {"launch_us": us, "achieved_gbs": gbs, "frac": gbs / peak}
+            b = plain_bytes + extra * rows
+            gbs = b / (us * 1e-6) / 1e9
+            out[k] = {"bytes_per_launch": b, "launch_us": us, "achieved_gbs": gbs, "frac": gbs / peak}
     return out
 
 
@@ -431,9 +436,9 @@ def run_ours(args):
                      "traffic": (traffic or {}).get("bytes_per_launch") if world == 1 else None,
                      "fem3_equiv_gbs": bytes_fem / t_spmv / 1e9,
                      "csr12_equiv_gbs": bytes_csr / t_spmv / 1e9, "launch_us": t_spmv * 1e6,
-                     # the two modes the BiCGSTAB iteration actually runs (85 % of the solve):
-                     # + D^-1 and r0 (or s) rows read, the Jacobi-scaled vector written
-                     "in_solve_modes": jacobi_roofline(kprof, bytes_alg + 16 * rows, peak) if grid_op else None},
+                     # the two modes the BiCGSTAB iteration actually runs (85 % of the step's
+                     # kernel time, profiles/r02_launches_bench_final_summary.json)
+                     "in_solve_modes": jacobi_roofline(kprof, bytes_alg, rows, peak) if grid_op else None},
         "newton": {"linear_method": args.linear, "iterations": rep.n_iterations,
                    "phase_s": getattr(rep, "timings", None),
                    "residual_norms": rep.residual_norms, "linear_iterations": lin_iters, "matvecs": matvecs,
