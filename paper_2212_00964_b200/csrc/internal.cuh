@@ -198,6 +198,7 @@ inline cudaError_t dalloc(T **p, size_t n) {
   return cudaMalloc((void **)p, (n ? n : 1) * sizeof(T));
 }
 int red_alloc(RedScratch *r);
+int xr_blocks();  // grid of k_update_xr (krylov.cu)
 void red_free(RedScratch *r);
 
 // ---------------------------------------------------------------- launchers

@@ -231,6 +231,29 @@ static int run_loop_graph(Matrix *m, LoopGraph &lg, F &&enqueue, b200fem_error *
 
 static int grid_vec(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + kThreads - 1) / kThreads)); }
 
+// Blocks of the reducing vector updates: one full wave.  k_update_xr needs 48 registers, so
+// 5 of its 256-thread blocks fit an SM; kRedBlocks (8 per SM) would run as a full wave plus a
+// 60 % one.  B200FEM_XR_BLOCKS=<n> overrides (<= kRedBlocks; the A/B switch).
+template <class K>
+static int wave_blocks(K kernel) {
+  int nb = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, 0) != cudaSuccess || nb <= 0) {
+    cudaGetLastError();
+    return kRedBlocks;
+  }
+  return std::min(kRedBlocks, nb * sms);
+}
+int xr_blocks() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("B200FEM_XR_BLOCKS");
+    v = e && atoi(e) > 0 ? std::min(atoi(e), kRedBlocks) : wave_blocks(k_update_xr);
+  }
+  return v;
+}
+
 static void enqueue_iteration(Matrix *m, const double *b, double *x) {
   KrylovWork *w = m->kw;
   cudaStream_t s = m->stream;
@@ -241,7 +264,7 @@ static void enqueue_iteration(Matrix *m, const double *b, double *x) {
   k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc);
   SpmvArgs a2{w->s, w->t, w->inv, w->diag, nullptr, nullptr, w->sc, 1};
   launch_spmv(m, SP_JACOBI_TT, a2, &w->red);
-  k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
+  k_update_xr<<<xr_blocks(), kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
   count_launch(3);
   (void)b;
 }
@@ -304,7 +327,7 @@ static int bicgstab_profile(Matrix *m, const double *b, double *x, int iters, do
         case 3: k_update_s<<<grid_vec(n), kThreads, 0, s>>>(n, w->r, w->v, w->s, w->sc); break;
         case 4: rc |= launch_spmv(m, SP_JACOBI_TT, a2, &w->red); break;
         case 5:
-          k_update_xr<<<kRedBlocks, kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
+          k_update_xr<<<xr_blocks(), kThreads, 0, s>>>(n, x, w->r, w->p, w->s, w->t, w->r0, w->diag, w->sc, w->red, 1);
           break;
         default: k_loop_status<<<1, 1, 0, s>>>(w->sc); break;
       }

@@ -294,7 +294,7 @@ static int enqueue_dist_iteration(Dist &D, double *const *x) {
     Part *P = D.parts[p];
     KrylovWork *w = P->m->kw;
     const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
-    k_update_xr<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, x[p] + lo, w->r + lo, w->p + lo, w->s + lo, w->t + lo,
+    k_update_xr<<<xr_blocks(), kThreads, 0, D.stream(p)>>>(n, x[p] + lo, w->r + lo, w->p + lo, w->s + lo, w->t + lo,
                                                          w->r0 + lo, w->diag + lo, w->sc, w->red, 0);
     count_launch();
   }
