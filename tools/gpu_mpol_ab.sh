@@ -1,5 +1,6 @@
 #!/bin/bash
 # L2 eviction priority of the matrix values (and x) in the Jacobi-mode GRID3 matvecs (A/B).
+# The B200FEM_GRID_MPOL variants were removed after this measurement (profiles/r02_mpol_ab.jsonl).
 set -u
 mkdir -p gpurun_out
 for i in 1 2; do
