@@ -193,7 +193,12 @@ class _NodeBlockOperator:
         and "grid32" Newton operators; each re-assembles into it before use)."""
         self._ws = ws
         self._n = ws.n_dofs
-        self.device_data = D.empty(getattr(ws, self._size)()) if data is None else data
+        # zero-filled once: lattice slots of missing neighbours are never written (the matvec
+        # masks them) and must not hold stale bits for value copies such as refresh_f32
+        if data is None:
+            with ws.on_stream():
+                data = D.zeros(getattr(ws, self._size)())
+        self.device_data = data
         self._handle = None
 
     @property
