@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -350,7 +351,6 @@ static int enqueue_dist_iteration_fused(Dist &D, double *const *x) {
     Part *P = D.parts[p];
     KrylovWork *w = P->m->kw;
     const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
-    if (!P->red6.partials && red_alloc(&P->red6)) return B200FEM_E_CUDA;
     RedScratch r6{P->red6.partials, P->red6.ticket, w->red.result + 2};
     k_dot6<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, w->r0 + lo, w->s + lo, w->t + lo, w->diag + lo, w->sc, r6);
     count_launch();
@@ -431,17 +431,31 @@ template <class F>
 static void capture_batch(Dist &D, BatchGraph &g, F &&enqueue_one) {
   g.tried = true;
   cudaStream_t s0 = D.stream(0);
+  const bool trace = getenv("B200FEM_KRYLOV_TRACE") != nullptr;
   for (size_t p = 1; p < D.parts.size(); ++p)
-    if (D.stream(p) != s0) return;
-  const int64_t l0 = g_launches.load();
-  cudaGraph_t graph = nullptr;
-  if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    if (D.stream(p) != s0) {
+      if (trace) fprintf(stderr, "[dist] batch graph not captured: parts on different streams\n");
+      return;
+    }
+  // capture needs a non-default stream (the parts' stream is usually the legacy one): the body
+  // is captured on a private stream (as krylov.cu run_loop_graph does), the graph runs on s0
+  static thread_local cudaStream_t cs = nullptr;
+  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
     return;
   }
+  const int64_t l0 = g_launches.load();
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    if (trace) fprintf(stderr, "[dist] batch graph not captured: cudaStreamBeginCapture failed\n");
+    return;
+  }
+  for (Part *P : D.parts) P->m->stream = cs;
   int st = 0;
   for (int i = 0; i < kDistGraphBatch; ++i) st |= enqueue_one();
-  cudaError_t e = cudaStreamEndCapture(s0, &graph);
+  for (Part *P : D.parts) P->m->stream = s0;
+  cudaError_t e = cudaStreamEndCapture(cs, &graph);
   g.launches = g_launches.load() - l0;
   count_launch(-(int)g.launches);  // captured, not launched
   if (st == 0 && e == cudaSuccess && graph) e = cudaGraphInstantiate(&g.exec, graph, 0);
@@ -451,6 +465,9 @@ static void capture_batch(Dist &D, BatchGraph &g, F &&enqueue_one) {
     g.exec = nullptr;
     cudaGetLastError();
   }
+  if (getenv("B200FEM_KRYLOV_TRACE"))
+    fprintf(stderr, "[dist] batch graph %s (%d iterations, %lld launches)\n", g.exec ? "captured" : "not captured: eager",
+            kDistGraphBatch, (long long)g.launches);
 }
 
 // Runs iterations until the device status leaves KS_RUNNING; `poll` is the pinned snapshot
@@ -591,6 +608,9 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
       count_launch();
     }
     const bool fused = dist_fused_dots(D);
+    if (fused)  // the fused dot group's scratch, allocated before any capture (no cudaMalloc inside one)
+      for (Part *P : D.parts)
+        if (!P->red6.partials && red_alloc(&P->red6)) return set_err(err, B200FEM_E_CUDA, "reduction scratch"), B200FEM_E_CUDA;
     if (int st = run_batches(D, graph, [&] { return fused ? enqueue_dist_iteration_fused(D, x)
                                                            : enqueue_dist_iteration(D, x); }, poll, err))
       return st;

@@ -186,13 +186,16 @@ print(sum(st.iterations for st in rep.linear_stats))
     res = {}
     with tempfile.TemporaryDirectory() as d:
         for fused in (True, False):
-            env = dict(os.environ, ROOT=root)
+            env = dict(os.environ, ROOT=root, B200FEM_KRYLOV_TRACE="1")
             env.pop("B200FEM_DIST_FUSED_DOTS", None)
+            env.pop("B200FEM_NO_GRAPH", None)
             if fused:
                 env["B200FEM_DIST_FUSED_DOTS"] = "1"
             f = os.path.join(d, f"u{int(fused)}.npy")
             r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=300)
             assert r.returncode == 0, r.stderr[-2000:]
+            # the iterations ran as the captured batch graph (no allocation inside the capture)
+            assert "[dist] batch graph captured" in r.stderr, r.stderr[-2000:]
             res[fused] = (np.load(f), int(r.stdout.strip().splitlines()[-1]))
     _, p1, _ = build("nh_block", dict(CASES["nh_block"], dims=(6, 5, 10)))
     U1, _ = fem.newton_solve(p1, **TIGHT)
