@@ -25,7 +25,9 @@ import tempfile
 import time
 
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # BLAS oversubscription
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # no "NCCL version" banner on stdout next to the JSON line
+# NCCL's log (its "NCCL version" banner included, when NCCL_DEBUG is set) goes to stderr, not to
+# stdout next to the JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
