@@ -25,9 +25,6 @@ import tempfile
 import time
 
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # BLAS oversubscription
-# NCCL's log (its "NCCL version" banner included, when NCCL_DEBUG is set) goes to stderr, not to
-# stdout next to the JSON line
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -468,7 +465,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_reference_sample(n)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist is not None:
         dist.destroy_process_group()
 
@@ -514,11 +511,24 @@ def run_reference(args):
                          "step_values_s": vals},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line, on the process's original stdout (see __main__)."""
+    os.write(_JSON_FD if _JSON_FD is not None else sys.stdout.fileno(), (json.dumps(obj) + "\n").encode())
 
 
 if __name__ == "__main__":
     a = parse()
     if "WORLD_SIZE" not in os.environ and (a.gpus > 1 or a.spawn):
         sys.exit(spawn_ranks(a))
+    # stdout carries exactly the JSON line: anything else written to fd 1 -- NCCL's
+    # "NCCL version" banner under NCCL_DEBUG=VERSION, library or Python prints -- goes to stderr
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     run_reference(a) if a.impl == "reference" else run_ours(a)
