@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256, MINB) k_tiles(const double *__restrict__ 
 // (d) the matvec's full value pattern: + the 13 lower blocks of node a read at node a - off_q
 // (L2 re-reads, two tiles per warp load); (e) + the 27 x gathers (3 doubles per neighbour).
 __constant__ int c_off[14];
-template <bool X>
+template <bool X, bool SOA = false>
 __global__ void __launch_bounds__(256, 1) k_full(const double *__restrict__ g, const double *__restrict__ x, int nch,
                                                  int nn, double *out) {
   const int lane = threadIdx.x & 31;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256, 1) k_full(const double *__restrict__ g, c
       for (int e = 0; e < 9; ++e) acc += __ldg(B + 32 * e);
       if (X)
 #pragma unroll
-        for (int t = 0; t < 3; ++t) acc += __ldg(x + 3L * m + t);
+        for (int t = 0; t < 3; ++t) acc += __ldg(SOA ? x + (long)t * nn + m : x + 3L * m + t);
     }
 #pragma unroll
     for (int q = 1; q < 14; ++q) {
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256, 1) k_full(const double *__restrict__ g, c
       for (int e = 0; e < 9; ++e) acc += __ldg(B + 32 * e);
       if (X)
 #pragma unroll
-        for (int t = 0; t < 3; ++t) acc += __ldg(x + 3L * m + t);
+        for (int t = 0; t < 3; ++t) acc += __ldg(SOA ? x + (long)t * nn + m : x + 3L * m + t);
     }
   }
   if (acc == 12345.678) *out = acc;
@@ -114,7 +114,9 @@ int main() {
   cudaMemset(x, 0, 3 * nodes * sizeof(double));
   const float tf = time_ms([&] { k_full<false><<<sms, 256>>>(g, x, (int)nch, (int)nodes, out); }, 20);
   const float tx = time_ms([&] { k_full<true><<<sms, 256>>>(g, x, (int)nch, (int)nodes, out); }, 20);
-  printf("{\"upper_lower_us\": %.1f, \"upper_lower_x_us\": %.1f}\n", tf * 1e3, tx * 1e3);
+  const float ts = time_ms([&] { k_full<true, true><<<sms, 256>>>(g, x, (int)nch, (int)nodes, out); }, 20);
+  printf("{\"upper_lower_us\": %.1f, \"upper_lower_x_us\": %.1f, \"upper_lower_x_soa_us\": %.1f}\n", tf * 1e3,
+         tx * 1e3, ts * 1e3);
   printf("{\"value_gb\": %.4f, \"linear_us\": %.1f, \"linear_gbs\": %.1f, \"tiles_1cta_us\": %.1f, \"tiles_1cta_gbs\": %.1f, "
          "\"tiles_2cta_us\": %.1f, \"tiles_2cta_gbs\": %.1f, \"tiles_4cta_us\": %.1f, \"tiles_4cta_gbs\": %.1f, \"err\": \"%s\"}\n",
          gb, t_lin * 1e3, gb / t_lin * 1e3, t1 * 1e3, gb / t1 * 1e3, t2 * 1e3, gb / t2 * 1e3, t4 * 1e3, gb / t4 * 1e3,
