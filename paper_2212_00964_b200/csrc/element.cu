@@ -775,7 +775,7 @@ struct Jac2Cfg {
 // `valid` false for padding lanes): on return lane (c, a) holds in K[d] the block of the pair
 // (a, (a + d) mod 8), d = 0..3 (and 4 for a < 4), as K_{(a,i),(b,k)}.  Element errors are
 // flagged on the device (DevErr) exactly as the other element kernels do.
-template <int MAT>
+template <int MAT, bool LOADED = false>
 __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, bool valid, int lane,
                                                  const double *__restrict__ sdN, double (*sXUw)[8][7], double *V,
                                                  double *Cf, double (&K)[5][Jac2Cfg<MAT>::VEC * Jac2Cfg<MAT>::VEC]) {
@@ -783,7 +783,7 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
   constexpr int VEC = CF::VEC, NV = CF::NV, QS = CF::QS, CS = CF::CS;
   constexpr int NB = 5, BB = VEC * VEC;
   const int c = lane >> 3, a8 = lane & 7;
-  {  // node a8 of cell c: coordinates and U
+  if (!LOADED) {  // node a8 of cell c: coordinates and U (LOADED: the caller staged them)
     const int node = a.cells[e * 8 + a8];
 #pragma unroll
     for (int d = 0; d < 3; ++d) sXUw[c][a8][d] = a.coords[(int64_t)node * 3 + d];
@@ -997,7 +997,11 @@ __device__ __forceinline__ void jac2_cell_blocks(const ElemArgs &a, int64_t e, b
   }
 }
 
-template <int MAT>
+// PF (default; B200FEM_JAC_NO_PF=1 is the A/B): each lane's node of the next batch (id, X, U)
+// is loaded into registers while the current batch computes, and staged into shared memory at
+// the top of the next iteration -- the batch-start gather latency off the critical path
+// (config 3: 6.76 -> 6.59 ms per NH tangent, bit-identical; profiles/r02_jacpf_ab.jsonl).
+template <int MAT, bool PF = false>
 __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, int64_t n, double *__restrict__ Ke,
                                                                     int soa) {
   using CF = Jac2Cfg<MAT>;
@@ -1013,11 +1017,29 @@ __global__ void __launch_bounds__(kJac2Warps * 32, 2) k_jacobian_v2(ElemArgs a, 
   double *Cf = jac2_sm + CF::SM_DN + CF::SM_XU + CF::SM_V + w * 160;         // [c][q][4], point stride 5
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double px[3] = {0.0, 0.0, 0.0}, pu[3] = {0.0, 0.0, 0.0};
+  auto load_node = [&](int64_t b) {  // this lane's node of the batch at b (clamped like e below)
+    const int64_t e2 = (b + c < n) ? b + c : n - 1;
+    const int node = a.cells[e2 * 8 + (lane & 7)];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) px[d] = a.coords[(int64_t)node * 3 + d];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) pu[v] = a.U[(int64_t)node * VEC + v];
+  };
+  if (PF && warp0 * 4 < n) load_node(warp0 * 4);
   for (int64_t base = warp0 * 4; base < n; base += nwarps * 4) {
     const bool valid = base + c < n;
     const int64_t e = valid ? base + c : n - 1;
     double K[NB][BB];
-    jac2_cell_blocks<MAT>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
+    if (PF) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) sXU[w][c][lane & 7][d] = px[d];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) sXU[w][c][lane & 7][3 + v] = pu[v];
+      if (base + nwarps * 4 < n) load_node(base + nwarps * 4);
+      __syncwarp();
+    }
+    jac2_cell_blocks<MAT, PF>(a, e, valid, lane, sdN, sXU[w], V, Cf, K);
     const int ia = lane & 7;
     if (soa) {
       // element-major scratch [pair][VV][cell] for the lattice pull: stage the warp's 4 cells
@@ -1582,6 +1604,18 @@ static void launch_jac2(int g, cudaStream_t s, const ElemArgs &a, int64_t n, dou
   if (!attr) {
     cudaFuncSetAttribute(k_jacobian_v2<MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Jac2Cfg<MAT>::BYTES);
     attr = true;
+  }
+  static int pf = -1;
+  if (pf < 0) pf = getenv("B200FEM_JAC_NO_PF") ? 0 : 1;
+  if (pf) {
+    static bool attr_pf = false;
+    if (!attr_pf) {
+      cudaFuncSetAttribute(k_jacobian_v2<MAT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)Jac2Cfg<MAT>::BYTES);
+      attr_pf = true;
+    }
+    k_jacobian_v2<MAT, true><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
+    return;
   }
   k_jacobian_v2<MAT><<<g, kJac2Warps * 32, Jac2Cfg<MAT>::BYTES, s>>>(a, n, Ke, soa);
 }
