@@ -2,10 +2,10 @@
 // (solvers.py:87-167), run on the device: all recurrence scalars (rho, alpha, omega,
 // beta, the iteration counter and the status) live in device memory and are updated by
 // the last block of each reduction, so the host never waits inside the inner loop.  The
-// host C++ loop only enqueues batches of iterations and polls the status of the
-// previous batch (double buffered), reproducing the outer restart loop: explicit
-// residual check, LinearSolverError at max_iters, restart on breakdown, BreakdownError
-// when a restart makes no progress.
+// inner loop is one CUDA-graph WHILE node per (re)start (run_loop_graph; B200FEM_NO_GRAPH=1:
+// batches of iterations with double-buffered status polling); the host C++ loop reproduces
+// the outer restart loop: explicit residual check, LinearSolverError at max_iters, restart
+// on breakdown, BreakdownError when a restart makes no progress.
 //
 // Per iteration (5 launches):
 //   K_a  p = r + beta (p - omega v)                                      (solvers.py:140)

@@ -5,9 +5,12 @@
 //   * a halo of the SpMV operand (p, then s): owned values of interface nodes -> the ghost
 //     entries of the neighbouring parts (packed, ncclSend/ncclRecv),
 //   * three FP64 sum-allreduces of the fused dot groups {r0.v}, {t.t, t.s},
-//     {||D r||^2, r0.r, r.r}, after which every part applies the same scalar update
-//     (Jacobi-PCG: one halo and two allreduces, {p.Ap}, {r.r, r.z}).
-// Batches of iterations run as one CUDA graph with the NCCL calls captured (run_batches).
+//     {||D r||^2, r0.r, r.r}, after which every part applies the same scalar update -- or
+//     two, the third group folded into the second by recurrence, from 4 NCCL ranks
+//     (enqueue_dist_iteration_fused) -- (Jacobi-PCG: one halo and two allreduces, {p.Ap},
+//     {r.r, r.z}).
+// Batches of iterations run as one CUDA graph with the NCCL calls captured on a private
+// stream (capture_batch, run_batches).
 // Communicators: NCCL across processes (one part per process and GPU), or "local": all
 // parts in one process on one device, exchanged by device copies and summed by a kernel
 // in part order -- the same algorithm, used to verify partitioning on a single B200.
