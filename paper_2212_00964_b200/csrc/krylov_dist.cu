@@ -321,6 +321,21 @@ static bool dist_fused_dots(const Dist &D) {
   return D.comm->kind == 1 && D.comm->nranks >= 4;
 }
 
+// k_dot6 in one full wave of resident blocks (42 registers: 5 per SM), as k_update_xr
+static int dot6_blocks() {
+  static int v = -1;
+  if (v < 0) {
+    int nb = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    v = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_dot6, kThreads, 0) == cudaSuccess && nb > 0)
+            ? std::min(kRedBlocks, nb * sms)
+            : kRedBlocks;
+    cudaGetLastError();
+  }
+  return v;
+}
+
 static int enqueue_dist_iteration_fused(Dist &D, double *const *x) {
   const size_t np = D.parts.size();
   std::vector<double *> pv(np), sv(np);
@@ -355,7 +370,7 @@ static int enqueue_dist_iteration_fused(Dist &D, double *const *x) {
     KrylovWork *w = P->m->kw;
     const int64_t lo = P->own_lo * P->vec, n = (P->own_hi - P->own_lo) * P->vec;
     RedScratch r6{P->red6.partials, P->red6.ticket, w->red.result + 2};
-    k_dot6<<<kRedBlocks, kThreads, 0, D.stream(p)>>>(n, w->r0 + lo, w->s + lo, w->t + lo, w->diag + lo, w->sc, r6);
+    k_dot6<<<dot6_blocks(), kThreads, 0, D.stream(p)>>>(n, w->r0 + lo, w->s + lo, w->t + lo, w->diag + lo, w->sc, r6);
     count_launch();
   }
   st |= D.allreduce(8);
@@ -614,6 +629,8 @@ static int dist_bicgstab(Dist &D, double *const *b, double *const *x, int has_x0
     if (fused)  // the fused dot group's scratch, allocated before any capture (no cudaMalloc inside one)
       for (Part *P : D.parts)
         if (!P->red6.partials && red_alloc(&P->red6)) return set_err(err, B200FEM_E_CUDA, "reduction scratch"), B200FEM_E_CUDA;
+    (void)xr_blocks();  // occupancy queries of the reducing updates, outside the capture too
+    if (fused) (void)dot6_blocks();
     if (int st = run_batches(D, graph, [&] { return fused ? enqueue_dist_iteration_fused(D, x)
                                                            : enqueue_dist_iteration(D, x); }, poll, err))
       return st;
