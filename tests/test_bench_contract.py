@@ -31,3 +31,29 @@ def test_reference_arm_prints_one_json_line():
     assert d["impl"] == "reference" and d["higher_is_better"] is False and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_helpers():
+    """In-solve roofline arithmetic and the partitioned allreduce count the bench line reports."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    kprof = {"kernels_us": {"spmv_jacobi_r0": 500.0, "spmv_jacobi_tt": 480.0}}
+    out = bench.jacobi_roofline(kprof, plain_bytes=2.7e9, rows=7.7e6, peak=6500.0)
+    r0, tt = out["spmv_jacobi_r0"], out["spmv_jacobi_tt"]
+    assert r0["bytes_per_launch"] == pytest.approx(2.7e9 + 16 * 7.7e6)  # + D^-1 and r0 rows
+    assert tt["bytes_per_launch"] == pytest.approx(2.7e9 + 8 * 7.7e6)   # + D^-1 rows
+    assert r0["achieved_gbs"] == pytest.approx(r0["bytes_per_launch"] / 500e-6 / 1e9)
+    assert tt["frac"] == pytest.approx(tt["achieved_gbs"] / 6500.0)
+    assert bench.jacobi_roofline(None, 1.0, 1.0, 1.0) is None
+    env = os.environ.pop("B200FEM_DIST_FUSED_DOTS", None)
+    try:
+        assert [bench.dist_allreduces(n) for n in (1, 2, 3, 4, 8)] == [3, 3, 3, 2, 2]
+        os.environ["B200FEM_DIST_FUSED_DOTS"] = "1"
+        assert bench.dist_allreduces(1) == 2
+        os.environ["B200FEM_DIST_FUSED_DOTS"] = "0"
+        assert bench.dist_allreduces(8) == 3
+    finally:
+        os.environ.pop("B200FEM_DIST_FUSED_DOTS", None)
+        if env is not None:
+            os.environ["B200FEM_DIST_FUSED_DOTS"] = env
